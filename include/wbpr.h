@@ -1,0 +1,191 @@
+/*
+ * wbpr.h — C ABI of libwbpr.so, the B200 (sm_100a) hot path of WBPR
+ * ("Engineering A Workload-balanced Push-Relabel Algorithm for Massive Graphs
+ * on GPUs", arXiv 2404.00270; PAPER.md in the reference tree).
+ *
+ * The library solves maximum flow / minimum cut (§2.1) with
+ * the vertex-centric lock-free push-relabel loop of Alg. 1 and
+ * Alg. 2 over the bidirectional / reversed CSR residual layouts of
+ * §3.2, entirely on the device:
+ *   A1 residual construction  (BCSR/RCSR + reverse-arc index by segmented sort)
+ *   A2 preflow                (Alg. 1 Step 0)
+ *   A3 active-vertex queue    (Alg. 2 lines 1-5)
+ *   A4 push/relabel           (Alg. 1 lines 9-21 with the relaxed rule P:187-189,
+ *                              one warp per active vertex)
+ *   A5 global relabel + termination, A6 gap heuristic
+ *   A7 device-resident loop   (one cooperative persistent kernel; no host polling)
+ *   A8 flow value e(t) and the canonical min-cut bitmap
+ *   A9 bipartite matching wrapper, A10 batches of disjoint instances.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns wbpr_status (0 = OK, < 0 = error) and never aborts the
+ *     process.  wbpr_last_error() returns a message for the last failure on the
+ *     calling thread.
+ *   - Synchronous: work is enqueued on `stream` (a cudaStream_t passed as void*,
+ *     NULL = legacy default stream), the call synchronises the stream once at the
+ *     end, and results are valid on return.
+ *   - Ownership: inputs are never written; the workspace is caller-allocated
+ *     device memory of at least wbpr_*_workspace_size() bytes (256-B aligned);
+ *     the library performs no cudaMalloc inside a solve.  One workspace serves
+ *     one solve at a time.
+ *   - Limits: vertex ids are int32 (n < 2^31); residual slots M < 2^31 and
+ *     2*m < 2^31; capacities are non-negative int32; flows are int64.
+ *   - Input rules: self-loops are ignored (counted); parallel edges are summed;
+ *     antiparallel edges share one arc pair in BCSR and stay distinct in RCSR;
+ *     zero capacities are allowed; rows may list their edges in any order.
+ *   - Bitmap: bit v lives in word v>>5 at bit position v&31 (LSB first);
+ *     padding bits >= n are 0; bit v = 1 <=> v is on the source side S*, where
+ *     S* = V \ {v : v reaches t in the final residual graph} (unique, §8(c)).
+ */
+#ifndef WBPR_H
+#define WBPR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t wbpr_status;
+#define WBPR_OK 0
+#define WBPR_EINVAL (-1)        /* bad argument or malformed graph (see stats.bad_edge_index) */
+#define WBPR_EOVERFLOW (-2)     /* merged capacity > INT32_MAX, or M / 2m >= 2^31 */
+#define WBPR_ENOMEM (-3)        /* workspace too small */
+#define WBPR_ECUDA (-4)         /* a CUDA runtime error; message in wbpr_last_error() */
+#define WBPR_ENOTCONVERGED (-5) /* round cap or watchdog timeout exceeded */
+#define WBPR_EINTERNAL (-6)     /* device certificate failed: cut capacity != e(t) */
+#define WBPR_ENOTIMPL (-7)
+
+/* Input graph in CSR form.  Edge i of row u is (u, col[i], cap[i]),
+ * i in [row_offsets[u], row_offsets[u+1]).  on_host = 0: the three arrays are
+ * DEVICE pointers; on_host = 1: HOST pointers (copied into the workspace inside
+ * the call, host->device time included in the call). */
+typedef struct wbpr_csr {
+  int64_t n;                  /* number of vertices, >= 2           */
+  int64_t m;                  /* number of edges, >= 0              */
+  const int64_t* row_offsets; /* [n+1], row_offsets[0]=0, [n]=m      */
+  const int32_t* col;         /* [m], 0 <= col < n                   */
+  const int32_t* cap;         /* [m], >= 0                           */
+  int32_t on_host;
+} wbpr_csr;
+
+#define WBPR_LAYOUT_BCSR 0
+#define WBPR_LAYOUT_RCSR 1
+
+typedef struct wbpr_options {
+  int32_t layout;        /* WBPR_LAYOUT_BCSR (default) or WBPR_LAYOUT_RCSR     */
+  float gr_beta;         /* global relabel when relabel work since the last GR exceeds
+                            gr_beta * (n + M) slots, or when the queue empties (P:178,
+                            P:374; reading §8(c) #8).  <= 0 -> default 0.5             */
+  int32_t gap_mode;      /* 0: gap by exact GR only; 1: + online height histogram (A6) */
+  int64_t max_rounds;    /* push/relabel round cap, 0 -> 10*n + 1000             */
+  int32_t grid_blocks;   /* persistent grid size, 0 -> all co-resident CTAs             */
+  int32_t timeout_ms;    /* device watchdog, 0 -> 120000                                 */
+  int32_t reserved[6];
+} wbpr_options;
+
+typedef struct wbpr_stats {
+  int64_t flow_value;        /* e(t) (sum over instances for a batch)                  */
+  int64_t cut_capacity;      /* sum of c over input edges S* -> V\S*                   */
+  int64_t n, m, M;           /* vertices, input edges, residual slots                  */
+  int64_t rounds;            /* push/relabel rounds (Alg. 2 iterations)                */
+  int64_t global_relabels;
+  int64_t bfs_levels;        /* BFS levels over all global relabels                    */
+  int64_t pushes, relabels;
+  int64_t arcs_scanned;      /* residual slots read by push/relabel scans              */
+  int64_t bfs_arcs_scanned;  /* residual slots read by global-relabel BFS              */
+  int64_t compaction_candidates; /* vertices examined by full AVQ compactions          */
+  int64_t avq_total;         /* sum of |AVQ| over rounds                                */
+  int64_t gap_lifts;         /* vertices lifted by the online gap heuristic            */
+  int64_t self_loops_ignored;
+  int64_t bad_edge_index;    /* first offending edge for EINVAL, else -1               */
+  int64_t excess_total;      /* Excess_total at termination              */
+  float build_ms, solve_ms, extract_ms, total_ms; /* CUDA-event times on `stream`       */
+  int32_t grid_blocks, block_threads;
+} wbpr_stats;
+
+/* Fill *opt with the defaults above. */
+wbpr_status wbpr_default_options(wbpr_options* opt);
+
+/* Bytes of device workspace a solve of a graph with n vertices and m edges needs
+ * (k instances for a batch; k = 1 otherwise). */
+wbpr_status wbpr_workspace_size(int64_t n, int64_t m, int32_t k, const wbpr_options* opt, size_t* bytes);
+
+/*
+ * wbpr_maxflow_solve — maximum flow value and canonical minimum cut of (g, s, t).
+ *   cut_bitmap: ceil(n/32) uint32 words, DEVICE (or HOST when g->on_host), caller-owned,
+ *               may be NULL.
+ *   stats:      HOST, may be NULL.
+ * Errors: EINVAL (n < 2, s == t, s/t out of range, cap < 0, col out of range, bad
+ * row offsets), EOVERFLOW, ENOMEM, ECUDA, ENOTCONVERGED, EINTERNAL.
+ */
+wbpr_status wbpr_maxflow_solve(const wbpr_csr* g, int64_t s, int64_t t, const wbpr_options* opt,
+                               void* workspace, size_t ws_bytes, uint32_t* cut_bitmap,
+                               wbpr_stats* stats, void* stream);
+
+/*
+ * wbpr_maxflow_solve_batch — k independent instances given as one disjoint-union
+ * CSR: instance i owns vertices [vbase[i], vbase[i+1]) and has terminals s[i], t[i]
+ * (HOST arrays).  Edges crossing instance ranges -> EINVAL.  flow_out / cutcap_out:
+ * HOST int64[k].  cut_bitmap covers the union graph (instance i = bits
+ * [vbase[i], vbase[i+1])).  All instances advance in the same rounds.
+ */
+wbpr_status wbpr_maxflow_solve_batch(const wbpr_csr* g, int32_t k, const int64_t* vbase,
+                                     const int64_t* s, const int64_t* t, const wbpr_options* opt,
+                                     void* workspace, size_t ws_bytes, uint32_t* cut_bitmap,
+                                     int64_t* flow_out, int64_t* cutcap_out, wbpr_stats* stats,
+                                     void* stream);
+
+/* Workspace for wbpr_bipartite_match. */
+wbpr_status wbpr_bipartite_workspace_size(int64_t nL, int64_t nR, int64_t E, const wbpr_options* opt,
+                                          size_t* bytes);
+
+/*
+ * wbpr_bipartite_match — maximum bipartite matching as maximum flow: the
+ * network is built on the device with s = 0, left l -> 1+l, right r -> 1+nL+r,
+ * t = nL+nR+1, unit capacities; duplicate (l, r) pairs are merged.
+ *   l, r:           DEVICE int32[E], 0 <= l < nL, 0 <= r < nR.
+ *   match_of_left:  DEVICE int32[nL], written: the matched right id or -1.
+ *   size_out:       HOST, the matching size (= max flow value).
+ */
+wbpr_status wbpr_bipartite_match(int64_t nL, int64_t nR, int64_t E, const int32_t* l, const int32_t* r,
+                                 const wbpr_options* opt, void* workspace, size_t ws_bytes,
+                                 int32_t* match_of_left, int64_t* size_out, wbpr_stats* stats,
+                                 void* stream);
+
+/* Debug/test view of the residual state left in a workspace by the last solve.
+ * All pointers are DEVICE pointers into the workspace.  BCSR: off/arc/mate/cap0 with
+ * arc[p] = {col, cf}.  RCSR: foff/farc/cap0 (forward), roff/rarc (rarc[q] = {col,
+ * flow_idx}), bcf (backward cf per forward arc).  e = excess (int64[n]),
+ * h = heights (int32[n], >= n means source side). */
+typedef struct wbpr_residual {
+  int32_t layout;
+  int64_t n, M, Mf;
+  const int32_t* off;   /* BCSR [n+1] / RCSR forward offsets [n+1] */
+  const int32_t* arc;   /* int2 pairs: BCSR [M] / RCSR forward [Mf] */
+  const int32_t* mate;  /* BCSR [M] */
+  const int32_t* cap0;  /* initial cf: BCSR [M] / RCSR forward [Mf] */
+  const int32_t* roff;  /* RCSR [n+1] */
+  const int32_t* rarc;  /* RCSR int2 [Mf] */
+  const int32_t* bcf;   /* RCSR [Mf] */
+  const int64_t* e;
+  const int32_t* h;
+} wbpr_residual;
+wbpr_status wbpr_residual_view(const void* workspace, wbpr_residual* view);
+
+/* Construction only (A1): builds the residual layout of g into the workspace
+ * and returns; wbpr_residual_view() then exposes it.  Used by the layout parity
+ * tests (bit-exact against the definition). */
+wbpr_status wbpr_build_residual(const wbpr_csr* g, const wbpr_options* opt, void* workspace,
+                                size_t ws_bytes, wbpr_stats* stats, void* stream);
+
+const char* wbpr_status_string(wbpr_status st);
+const char* wbpr_last_error(void);
+/* Library version string, e.g. "wbpr 0.1 sm_100a". */
+const char* wbpr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WBPR_H */

@@ -122,3 +122,39 @@ def demerge_bcsr(n, row_off, col, cap, off, arc_col, cf, cap0, mate):
     if any(v != 0 for v in remaining.values()):
         raise CheckError("demerge: net flow exceeds the parallel-edge capacities")
     return f
+
+
+def demerge_rcsr(n, row_off, col, cap, foff, fcol, fcf, cap0, bcf):
+    """Per-input-edge flows from an RCSR residual state: forward arc p carries
+    flow cap0[p] - fcf[p] (= bcf[p]); assigned greedily to its parallel input edges."""
+    foff = np.asarray(foff, np.int64)
+    fcol = np.asarray(fcol, np.int64)
+    fcf = np.asarray(fcf, np.int64)
+    cap0 = np.asarray(cap0, np.int64)
+    bcf = np.asarray(bcf, np.int64)
+    if np.any(fcf < 0) or np.any(bcf < 0):
+        raise CheckError("V1(rcsr): negative residual capacity")
+    if np.any(fcf + bcf != cap0):
+        raise CheckError("V1(rcsr): forward + backward cf != capacity")
+    owner = np.repeat(np.arange(n, dtype=np.int64), np.diff(foff))
+    key = owner * n + fcol
+    x = cap0 - fcf
+    src = _edges(n, row_off)
+    col = np.asarray(col, np.int64)
+    cap = np.asarray(cap, np.int64)
+    f = np.zeros(col.shape[0], np.int64)
+    pos = np.searchsorted(key, src * n + col)
+    remaining = {}
+    for i in range(col.shape[0]):
+        if src[i] == col[i]:
+            continue
+        p = int(pos[i])
+        if p >= key.shape[0] or key[p] != src[i] * n + col[i]:
+            raise CheckError(f"demerge: input edge {i} has no RCSR arc")
+        r = remaining.setdefault(p, int(x[p]))
+        d = min(r, int(cap[i]))
+        f[i] = d
+        remaining[p] = r - d
+    if any(v != 0 for v in remaining.values()):
+        raise CheckError("demerge: arc flow exceeds its parallel-edge capacities")
+    return f

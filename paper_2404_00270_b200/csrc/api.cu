@@ -1,0 +1,510 @@
+// api.cu — the C ABI of libwbpr.so (declared in include/wbpr.h): argument
+// validation, workspace carving, launch orchestration and error mapping.
+// Each solve: K-BUILD kernels (A1) -> one cooperative persistent kernel (A2-A7)
+// -> extraction kernels (A8) -> one stream synchronisation.
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "wbpr.h"
+#include "internal.h"
+#include "kernels.h"
+
+using namespace wbpr;
+
+namespace {
+
+thread_local std::string g_err;
+
+wbpr_status fail(wbpr_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CK(call)                                                                                      \
+  do {                                                                                                \
+    cudaError_t _e = (call);                                                                          \
+    if (_e != cudaSuccess) {                                                                          \
+      return fail(WBPR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));                    \
+    }                                                                                                 \
+  } while (0)
+
+struct DevInfo {
+  int num_sms = 0;
+  int occ[2] = {0, 0};
+};
+
+std::mutex g_mu;
+std::unordered_map<int, DevInfo> g_dev;
+std::unordered_map<const void*, wbpr_residual> g_views;
+
+wbpr_status dev_info(DevInfo& out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_dev.find(dev);
+  if (it != g_dev.end()) { out = it->second; return WBPR_OK; }
+  DevInfo d;
+  CK(cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  d.occ[0] = solve_max_blocks_per_sm(0, kSolveThreads);
+  d.occ[1] = solve_max_blocks_per_sm(1, kSolveThreads);
+  CK(cudaGetLastError());
+  g_dev[dev] = d;
+  out = d;
+  return WBPR_OK;
+}
+
+__global__ void k_init_ctrl(Ctrl* c) {
+  int* p = reinterpret_cast<int*>(c);
+  for (size_t i = threadIdx.x; i < sizeof(Ctrl) / sizeof(int); i += blockDim.x) p[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) c->bad_edge = LLONG_MAX;
+}
+
+__global__ void k_terms(uint8_t* term, const long long* s, const long long* t, int k) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x) {
+    term[s[i]] = kSource;
+    term[t[i]] = kSink;
+  }
+}
+
+// batch: every edge must stay inside its instance's vertex range (A10)
+__global__ void k_check_ranges(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
+                               const int64_t* __restrict__ vbase, int k, Ctrl* ctrl) {
+  for (int i = blockIdx.x; i < k; i += gridDim.x) {
+    int64_t lo = vbase[i], hi = vbase[i + 1];
+    for (int64_t e = ro[lo] + threadIdx.x; e < ro[hi]; e += blockDim.x) {
+      int v = col[e];
+      if (v < lo || v >= hi) atomicMin((unsigned long long*)&ctrl->bad_edge, (unsigned long long)e);
+    }
+  }
+}
+
+template <typename T> T* at(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
+
+struct Ws {
+  Layout L;
+  void* base;
+  Ctrl* ctrl;
+};
+
+wbpr_status read_ctrl(const Ctrl* d, Ctrl& h, cudaStream_t st) {
+  CK(cudaMemcpyAsync(&h, d, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return WBPR_OK;
+}
+
+wbpr_options resolve(const wbpr_options* o) {
+  wbpr_options r;
+  wbpr_default_options(&r);
+  if (o) r = *o;
+  if (!(r.gr_beta > 0.f)) r.gr_beta = 0.5f;
+  if (r.timeout_ms <= 0) r.timeout_ms = 120000;
+  return r;
+}
+
+// A1 for one workspace; fills M / Mf.  `ro,col,cap` are device pointers.
+wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, const int32_t* cap, int layout,
+                           int num_sms, int& M, int& Mf, int64_t& selfloops, int64_t& bad_edge, cudaStream_t st) {
+  const Layout& L = W.L;
+  BuildArgs a{};
+  a.n = L.n; a.m = L.m; a.layout = layout; a.num_sms = num_sms;
+  a.ro = ro; a.col = col; a.cap = cap; a.ctrl = W.ctrl;
+  a.deg = at<int>(W.base, L.deg); a.cursor = at<int>(W.base, L.cursor);
+  a.soff = at<int>(W.base, L.soff); a.off = at<int>(W.base, L.off); a.roff = at<int>(W.base, L.roff);
+  a.scan_part = at<int>(W.base, L.scan_part); a.q0 = at<int>(W.base, L.q0);
+  a.keys = at<uint64_t>(W.base, L.regA); a.tmp = at<uint64_t>(W.base, L.regB);
+  a.arc = at<int2>(W.base, L.regC);
+  a.mate = at<int>(W.base, L.regB);
+  a.cap0 = at<int>(W.base, L.regB + L.bcap0);
+  a.rarc = at<int2>(W.base, L.regC + 8 * (size_t)L.m);
+  a.bcf = at<int>(W.base, L.regB);
+
+  build_validate(a, st);
+  CK(cudaGetLastError());
+  Ctrl c;
+  wbpr_status s = read_ctrl(W.ctrl, c, st);
+  if (s) return s;
+  selfloops = c.selfloops;
+  bad_edge = c.bad_edge == LLONG_MAX ? -1 : c.bad_edge;
+  if (c.bad_rows) return fail(WBPR_EINVAL, "row_offsets are not a valid CSR offset array");
+  if (bad_edge >= 0)
+    return fail(WBPR_EINVAL, "edge " + std::to_string(bad_edge) + " has an out-of-range column or a negative capacity");
+  a.maxlen = c.maxlen;
+  if (layout == WBPR_LAYOUT_BCSR) {
+    a.H = 2 * L.m - c.selfloops;
+    build_bcsr(a, st);
+    CK(cudaGetLastError());
+    s = read_ctrl(W.ctrl, c, st);
+    if (s) return s;
+    M = c.M; Mf = c.M;
+    if (c.overflow == 1) return fail(WBPR_EOVERFLOW, "merged capacity exceeds INT32_MAX");
+    build_bcsr_mate(a, M, st);
+    CK(cudaGetLastError());
+    s = read_ctrl(W.ctrl, c, st);
+    if (s) return s;
+    if (c.overflow == 2) return fail(WBPR_EINTERNAL, "reverse arc not found while building mate[]");
+  } else {
+    a.H = L.m;
+    build_rcsr_forward(a, st);
+    CK(cudaGetLastError());
+    s = read_ctrl(W.ctrl, c, st);
+    if (s) return s;
+    if (c.overflow == 1) return fail(WBPR_EOVERFLOW, "merged capacity exceeds INT32_MAX");
+    Mf = c.M;
+    build_rcsr_reverse_counts(a, Mf, st);
+    CK(cudaGetLastError());
+    s = read_ctrl(W.ctrl, c, st);
+    if (s) return s;
+    build_rcsr_reverse(a, Mf, c.maxlen, st);
+    CK(cudaGetLastError());
+    M = 2 * Mf;
+  }
+  return WBPR_OK;
+}
+
+void register_view(const Ws& W, int layout, int M, int Mf) {
+  const Layout& L = W.L;
+  wbpr_residual v{};
+  v.layout = layout;
+  v.n = L.n; v.M = M; v.Mf = Mf;
+  v.off = at<int>(W.base, L.off);
+  v.arc = at<int>(W.base, L.regC);
+  v.cap0 = at<int>(W.base, L.regB + L.bcap0);
+  if (layout == WBPR_LAYOUT_BCSR) {
+    v.mate = at<int>(W.base, L.regB);
+  } else {
+    v.roff = at<int>(W.base, L.roff);
+    v.rarc = at<int>(W.base, L.regC + 8 * (size_t)L.m);
+    v.bcf = at<int>(W.base, L.regB);
+  }
+  v.e = at<int64_t>(W.base, L.e);
+  v.h = at<int32_t>(W.base, L.h);
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_views[W.base] = v;
+}
+
+wbpr_status check_graph_args(const wbpr_csr* g) {
+  if (!g) return fail(WBPR_EINVAL, "graph is NULL");
+  if (g->n < 2) return fail(WBPR_EINVAL, "n must be >= 2");
+  if (g->n >= INT32_MAX) return fail(WBPR_EOVERFLOW, "n must be < 2^31");
+  if (g->m < 0) return fail(WBPR_EINVAL, "m must be >= 0");
+  if (2 * g->m >= INT32_MAX) return fail(WBPR_EOVERFLOW, "2*m must be < 2^31");
+  if (!g->row_offsets || (g->m > 0 && (!g->col || !g->cap))) return fail(WBPR_EINVAL, "NULL CSR array");
+  return WBPR_OK;
+}
+
+struct Events {
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  ~Events() { for (auto& e : ev) if (e) cudaEventDestroy(e); }
+  cudaError_t create() {
+    for (auto& e : ev) { cudaError_t r = cudaEventCreate(&e); if (r) return r; }
+    return cudaSuccess;
+  }
+};
+
+// Shared driver of single and batch solves.
+wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const int64_t* s_h, const int64_t* t_h,
+                       const wbpr_options* opt_in, void* ws, size_t ws_bytes, uint32_t* bitmap, int64_t* flow_out,
+                       int64_t* cut_out, wbpr_stats* stats, cudaStream_t st, bool build_only) {
+  wbpr_status s = check_graph_args(g);
+  if (s) return s;
+  wbpr_options opt = resolve(opt_in);
+  if (opt.layout != WBPR_LAYOUT_BCSR && opt.layout != WBPR_LAYOUT_RCSR) return fail(WBPR_EINVAL, "unknown layout");
+  const int64_t n = g->n, m = g->m;
+  if (k < 1 || k > kMaxInst) return fail(WBPR_EINVAL, "instance count out of range");
+  if (vbase_h[0] != 0 || vbase_h[k] != n) return fail(WBPR_EINVAL, "vbase must start at 0 and end at n");
+  for (int i = 0; i < k; ++i) {
+    if (vbase_h[i + 1] <= vbase_h[i]) return fail(WBPR_EINVAL, "vbase must be increasing");
+    if (s_h[i] < vbase_h[i] || s_h[i] >= vbase_h[i + 1] || t_h[i] < vbase_h[i] || t_h[i] >= vbase_h[i + 1])
+      return fail(WBPR_EINVAL, "terminal out of its instance range");
+    if (s_h[i] == t_h[i]) return fail(WBPR_EINVAL, "s == t");
+  }
+  if (!ws) return fail(WBPR_EINVAL, "workspace is NULL");
+  Ws W;
+  W.L = make_layout(n, m, k, opt.layout);
+  if (ws_bytes < W.L.total)
+    return fail(WBPR_ENOMEM, "workspace too small: need " + std::to_string(W.L.total) + " bytes");
+  W.base = ws;
+  W.ctrl = at<Ctrl>(ws, W.L.ctrl);
+  DevInfo di;
+  s = dev_info(di);
+  if (s) return s;
+  const Layout& L = W.L;
+
+  Events E;
+  CK(E.create());
+  CK(cudaEventRecord(E.ev[0], st));
+
+  const int64_t* ro = g->row_offsets;
+  const int32_t* col = g->col;
+  const int32_t* cap = g->cap;
+  if (g->on_host) {
+    CK(cudaMemcpyAsync(at<int64_t>(ws, L.in_row), ro, 8 * (n + 1), cudaMemcpyHostToDevice, st));
+    if (m > 0) {
+      CK(cudaMemcpyAsync(at<int32_t>(ws, L.in_col), col, 4 * m, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(at<int32_t>(ws, L.in_cap), cap, 4 * m, cudaMemcpyHostToDevice, st));
+    }
+    ro = at<int64_t>(ws, L.in_row);
+    col = at<int32_t>(ws, L.in_col);
+    cap = at<int32_t>(ws, L.in_cap);
+  }
+  k_init_ctrl<<<1, 256, 0, st>>>(W.ctrl);
+  long long* d_s = at<long long>(ws, L.inst_s);
+  long long* d_t = at<long long>(ws, L.inst_t);
+  int64_t* d_vb = at<int64_t>(ws, L.vbase);
+  CK(cudaMemcpyAsync(d_s, s_h, 8 * k, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_t, t_h, 8 * k, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_vb, vbase_h, 8 * (k + 1), cudaMemcpyHostToDevice, st));
+  uint8_t* term = at<uint8_t>(ws, L.term);
+  CK(cudaMemsetAsync(term, 0, n, st));
+  k_terms<<<(k + 255) / 256, 256, 0, st>>>(term, d_s, d_t, k);
+  if (k > 1) k_check_ranges<<<std::min(k, di.num_sms * 8), 256, 0, st>>>(ro, col, n, d_vb, k, W.ctrl);
+  CK(cudaGetLastError());
+
+  int M = 0, Mf = 0;
+  int64_t selfloops = 0, bad_edge = -1;
+  s = build_residual(W, ro, col, cap, opt.layout, di.num_sms, M, Mf, selfloops, bad_edge, st);
+  if (stats) { memset(stats, 0, sizeof(*stats)); stats->bad_edge_index = bad_edge; stats->n = n; stats->m = m; }
+  if (s) return s;
+  register_view(W, opt.layout, M, Mf);
+  CK(cudaEventRecord(E.ev[1], st));
+  if (build_only) {
+    CK(cudaStreamSynchronize(st));
+    if (stats) {
+      stats->M = M; stats->self_loops_ignored = selfloops;
+      float ms = 0; cudaEventElapsedTime(&ms, E.ev[0], E.ev[1]); stats->build_ms = ms; stats->total_ms = ms;
+    }
+    return WBPR_OK;
+  }
+
+  SolveParams P{};
+  P.ctrl = W.ctrl;
+  P.n = (int)n; P.k = k; P.layout = opt.layout; P.M = M; P.Mf = Mf;
+  P.off = at<int>(ws, L.off);
+  P.arc = at<int2>(ws, L.regC);
+  P.mate = at<int>(ws, L.regB);
+  P.roff = at<int>(ws, L.roff);
+  P.rarc = at<int2>(ws, L.regC + 8 * (size_t)m);
+  P.bcf = at<int>(ws, L.regB);
+  P.h = at<int>(ws, L.h);
+  P.e = at<long long>(ws, L.e);
+  P.term = term;
+  P.deact = at<uint8_t>(ws, L.deact);
+  P.q[0] = at<int>(ws, L.q0); P.q[1] = at<int>(ws, L.q1);
+  P.hq[0] = at<HugeRec>(ws, L.hq0); P.hq[1] = at<HugeRec>(ws, L.hq1);
+  P.hc[0] = at<int2>(ws, L.hc0); P.hc[1] = at<int2>(ws, L.hc1);
+  P.hist = at<int>(ws, L.hist);
+  P.src = d_s; P.snk = d_t;
+  P.max_rounds = opt.max_rounds > 0 ? opt.max_rounds : 10 * n + 1000;
+  P.gr_threshold = (unsigned long long)((double)opt.gr_beta * (double)(n + M)) + 1;
+  P.gap_mode = opt.gap_mode;
+  P.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
+  int occ = di.occ[opt.layout];
+  if (occ < 1) return fail(WBPR_ECUDA, "solve kernel cannot be resident on this device");
+  int blocks = di.num_sms * occ;
+  if (opt.grid_blocks > 0 && opt.grid_blocks < blocks) blocks = opt.grid_blocks;
+  CK(launch_solve(P, blocks, kSolveThreads, st));
+  CK(cudaEventRecord(E.ev[2], st));
+
+  uint32_t* dbm = bitmap;
+  if (bitmap && g->on_host) dbm = reinterpret_cast<uint32_t*>(at<int>(ws, L.q0));
+  long long* d_flow = at<long long>(ws, L.inst_flow);
+  long long* d_cut = at<long long>(ws, L.inst_cut);
+  extract_results(P, ro, col, cap, m, dbm, d_vb, k, d_flow, d_cut, di.num_sms, st);
+  CK(cudaGetLastError());
+  std::vector<long long> hf(k), hc(k);
+  CK(cudaMemcpyAsync(hf.data(), d_flow, 8 * k, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hc.data(), d_cut, 8 * k, cudaMemcpyDeviceToHost, st));
+  if (bitmap && g->on_host)
+    CK(cudaMemcpyAsync(bitmap, dbm, 4 * ((n + 31) / 32), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(E.ev[3], st));
+  Ctrl c;
+  CK(cudaMemcpyAsync(&c, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+
+  long long F = 0, C = 0;
+  bool cert = true;
+  for (int i = 0; i < k; ++i) {
+    F += hf[i]; C += hc[i];
+    if (hf[i] != hc[i]) cert = false;
+    if (flow_out) flow_out[i] = hf[i];
+    if (cut_out) cut_out[i] = hc[i];
+  }
+  if (stats) {
+    stats->flow_value = F;
+    stats->cut_capacity = C;
+    stats->M = M;
+    stats->rounds = c.stats[ST_ROUNDS];
+    stats->global_relabels = c.stats[ST_GRS];
+    stats->bfs_levels = c.stats[ST_BFS_LEVELS];
+    stats->pushes = c.stats[ST_PUSHES];
+    stats->relabels = c.stats[ST_RELABELS];
+    stats->arcs_scanned = c.stats[ST_ARCS];
+    stats->bfs_arcs_scanned = c.stats[ST_BFS_ARCS];
+    stats->compaction_candidates = c.stats[ST_CAND];
+    stats->avq_total = c.stats[ST_AVQ];
+    stats->gap_lifts = c.stats[ST_GAPLIFT];
+    stats->self_loops_ignored = selfloops;
+    stats->excess_total = c.excess_total;
+    float ms;
+    cudaEventElapsedTime(&ms, E.ev[0], E.ev[1]); stats->build_ms = ms;
+    cudaEventElapsedTime(&ms, E.ev[1], E.ev[2]); stats->solve_ms = ms;
+    cudaEventElapsedTime(&ms, E.ev[2], E.ev[3]); stats->extract_ms = ms;
+    cudaEventElapsedTime(&ms, E.ev[0], E.ev[3]); stats->total_ms = ms;
+    stats->grid_blocks = blocks;
+    stats->block_threads = kSolveThreads;
+  }
+  if (c.status == DS_NOTCONVERGED) return fail(WBPR_ENOTCONVERGED, "round cap exceeded");
+  if (c.abort) return fail(WBPR_ENOTCONVERGED, "device watchdog timeout");
+  if (!cert) return fail(WBPR_EINTERNAL, "certificate failed: cut capacity != flow value");
+  // Paper's termination identity: e(s) + e(t) >= Excess_total at the end.
+  if (F != c.excess_total) return fail(WBPR_EINTERNAL, "Excess_total bookkeeping disagrees with e(t)");
+  return WBPR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+wbpr_status wbpr_default_options(wbpr_options* opt) {
+  if (!opt) return fail(WBPR_EINVAL, "NULL options");
+  memset(opt, 0, sizeof(*opt));
+  opt->layout = WBPR_LAYOUT_BCSR;
+  opt->gr_beta = 0.5f;
+  opt->gap_mode = 0;
+  opt->max_rounds = 0;
+  opt->grid_blocks = 0;
+  opt->timeout_ms = 120000;
+  return WBPR_OK;
+}
+
+wbpr_status wbpr_workspace_size(int64_t n, int64_t m, int32_t k, const wbpr_options* opt, size_t* bytes) {
+  if (!bytes) return fail(WBPR_EINVAL, "NULL bytes");
+  if (n < 2 || m < 0 || k < 1) return fail(WBPR_EINVAL, "bad sizes");
+  if (n >= INT32_MAX || 2 * m >= INT32_MAX) return fail(WBPR_EOVERFLOW, "size beyond int32 indexing");
+  wbpr_options o = resolve(opt);
+  *bytes = make_layout(n, m, k, o.layout).total;
+  return WBPR_OK;
+}
+
+wbpr_status wbpr_maxflow_solve(const wbpr_csr* g, int64_t s, int64_t t, const wbpr_options* opt, void* workspace,
+                               size_t ws_bytes, uint32_t* cut_bitmap, wbpr_stats* stats, void* stream) {
+  if (!g) return fail(WBPR_EINVAL, "graph is NULL");
+  if (s < 0 || t < 0 || s >= g->n || t >= g->n) return fail(WBPR_EINVAL, "s or t out of range");
+  if (s == t) return fail(WBPR_EINVAL, "s == t");
+  int64_t vb[2] = {0, g->n};
+  return solve_impl(g, 1, vb, &s, &t, opt, workspace, ws_bytes, cut_bitmap, nullptr, nullptr, stats,
+                    (cudaStream_t)stream, false);
+}
+
+wbpr_status wbpr_maxflow_solve_batch(const wbpr_csr* g, int32_t k, const int64_t* vbase, const int64_t* s,
+                                     const int64_t* t, const wbpr_options* opt, void* workspace, size_t ws_bytes,
+                                     uint32_t* cut_bitmap, int64_t* flow_out, int64_t* cutcap_out, wbpr_stats* stats,
+                                     void* stream) {
+  if (!vbase || !s || !t) return fail(WBPR_EINVAL, "NULL batch arrays");
+  return solve_impl(g, k, vbase, s, t, opt, workspace, ws_bytes, cut_bitmap, flow_out, cutcap_out, stats,
+                    (cudaStream_t)stream, false);
+}
+
+wbpr_status wbpr_build_residual(const wbpr_csr* g, const wbpr_options* opt, void* workspace, size_t ws_bytes,
+                                wbpr_stats* stats, void* stream) {
+  if (!g) return fail(WBPR_EINVAL, "graph is NULL");
+  int64_t vb[2] = {0, g->n};
+  int64_t s = 0, t = g->n - 1;
+  return solve_impl(g, 1, vb, &s, &t, opt, workspace, ws_bytes, nullptr, nullptr, nullptr, stats,
+                    (cudaStream_t)stream, true);
+}
+
+wbpr_status wbpr_bipartite_workspace_size(int64_t nL, int64_t nR, int64_t E, const wbpr_options* opt, size_t* bytes) {
+  if (nL < 0 || nR < 0 || E < 0) return fail(WBPR_EINVAL, "bad sizes");
+  return wbpr_workspace_size(nL + nR + 2, nL + E + nR, 1, opt, bytes);
+}
+
+wbpr_status wbpr_bipartite_match(int64_t nL, int64_t nR, int64_t E, const int32_t* l, const int32_t* r,
+                                 const wbpr_options* opt_in, void* workspace, size_t ws_bytes, int32_t* match_of_left,
+                                 int64_t* size_out, wbpr_stats* stats, void* stream) {
+  if (nL < 0 || nR < 0 || E < 0) return fail(WBPR_EINVAL, "bad sizes");
+  if (E > 0 && (!l || !r)) return fail(WBPR_EINVAL, "NULL edge arrays");
+  if (!workspace) return fail(WBPR_EINVAL, "workspace is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  wbpr_options opt = resolve(opt_in);
+  const int64_t n = nL + nR + 2, m = nL + E + nR;
+  if (2 * m >= INT32_MAX || n >= INT32_MAX) return fail(WBPR_EOVERFLOW, "size beyond int32 indexing");
+  Layout L = make_layout(n, m, 1, opt.layout);
+  if (ws_bytes < L.total) return fail(WBPR_ENOMEM, "workspace too small: need " + std::to_string(L.total) + " bytes");
+  DevInfo di;
+  wbpr_status s = dev_info(di);
+  if (s) return s;
+  Ctrl* ctrl = at<Ctrl>(workspace, L.ctrl);
+  int* deg = at<int>(workspace, L.deg);
+  int* cursor = at<int>(workspace, L.cursor);
+  int64_t* ro = at<int64_t>(workspace, L.in_row);
+  int32_t* col = at<int32_t>(workspace, L.in_col);
+  int32_t* cap = at<int32_t>(workspace, L.in_cap);
+  k_init_ctrl<<<1, 256, 0, st>>>(ctrl);
+  bip_validate(nL, nR, E, l, r, deg, cursor, ctrl, di.num_sms, st);
+  CK(cudaGetLastError());
+  Ctrl c;
+  s = read_ctrl(ctrl, c, st);
+  if (s) return s;
+  if (c.bad_edge != LLONG_MAX) {
+    if (stats) { memset(stats, 0, sizeof(*stats)); stats->bad_edge_index = c.bad_edge; }
+    return fail(WBPR_EINVAL, "edge " + std::to_string(c.bad_edge) + " has an id outside its side");
+  }
+  bip_build(nL, nR, E, l, r, ro, col, cap, deg, cursor, at<int>(workspace, L.scan_part), di.num_sms, st);
+  CK(cudaGetLastError());
+  wbpr_csr g{n, m, ro, col, cap, 0};
+  int64_t vb[2] = {0, n};
+  int64_t sv = 0, tv = n - 1;
+  int64_t F = 0;
+  s = solve_impl(&g, 1, vb, &sv, &tv, &opt, workspace, ws_bytes, nullptr, &F, nullptr, stats, st, false);
+  if (s) return s;
+  SolveParams P{};
+  P.layout = opt.layout;
+  P.off = at<int>(workspace, L.off);
+  P.arc = at<int2>(workspace, L.regC);
+  P.roff = at<int>(workspace, L.roff);
+  P.rarc = at<int2>(workspace, L.regC + 8 * (size_t)m);
+  P.bcf = at<int>(workspace, L.regB);
+  if (match_of_left && nL > 0) {
+    bip_extract(P, nL, nR, match_of_left, di.num_sms, st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+  }
+  if (size_out) *size_out = F;
+  return WBPR_OK;
+}
+
+wbpr_status wbpr_residual_view(const void* workspace, wbpr_residual* view) {
+  if (!workspace || !view) return fail(WBPR_EINVAL, "NULL argument");
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_views.find(workspace);
+  if (it == g_views.end()) return fail(WBPR_EINVAL, "no residual has been built in this workspace");
+  *view = it->second;
+  return WBPR_OK;
+}
+
+const char* wbpr_status_string(wbpr_status st) {
+  switch (st) {
+    case WBPR_OK: return "WBPR_OK";
+    case WBPR_EINVAL: return "WBPR_EINVAL";
+    case WBPR_EOVERFLOW: return "WBPR_EOVERFLOW";
+    case WBPR_ENOMEM: return "WBPR_ENOMEM";
+    case WBPR_ECUDA: return "WBPR_ECUDA";
+    case WBPR_ENOTCONVERGED: return "WBPR_ENOTCONVERGED";
+    case WBPR_EINTERNAL: return "WBPR_EINTERNAL";
+    case WBPR_ENOTIMPL: return "WBPR_ENOTIMPL";
+    default: return "WBPR_UNKNOWN";
+  }
+}
+
+const char* wbpr_last_error(void) { return g_err.c_str(); }
+
+const char* wbpr_version(void) { return "wbpr 0.1 sm_100a"; }
+
+}  // extern "C"

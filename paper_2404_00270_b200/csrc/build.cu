@@ -1,0 +1,322 @@
+// build.cu — K-BUILD (A1): device-side construction of the residual layouts of
+// PAPER.md §3.2 (Fig. 2):
+//   BCSR  one merged, column-sorted segment per vertex with its in- and out-arcs
+//          plus mate[p] = slot of the reverse arc: the paper's per-push
+//         binary search done once here (reading §8(c) #12).
+//   RCSR  forward CSR + reversed CSR whose entries carry flow_idx.
+// Readings: parallel edges summed, antiparallel pairs share one BCSR arc
+// pair, self-loops dropped and counted, zero-capacity pairs kept.
+#include <climits>
+
+#include "internal.h"
+#include "kernels.h"
+
+namespace wbpr {
+
+constexpr uint64_t kSent = ~0ull;  // self-loop / invalid half-arc: sorts last, never a head
+
+__device__ __forceinline__ int64_t row_of(const int64_t* __restrict__ ro, int64_t n, int64_t i) {
+  // largest u with ro[u] <= i  (ro non-decreasing, ro[0] = 0)
+  int64_t lo = 0, hi = n;  // answer in [0, n)
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(ro + mid) <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int row_of32(const int* __restrict__ off, int n, int i) {
+  int lo = 0, hi = n;
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (__ldg(off + mid) <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// Row-offset sanity + raw out-degrees (self-loops included as sentinel slots).
+__global__ void k_rows(const int64_t* __restrict__ ro, int64_t n, int64_t m, int* deg, Ctrl* ctrl) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = ro[u], b = ro[u + 1];
+    bool bad = a > b || a < 0 || b > m || (u == 0 && a != 0) || (u == n - 1 && b != m);
+    if (bad) atomicExch(&ctrl->bad_rows, 1);
+    deg[u] = bad ? 0 : (int)(b - a);
+  }
+}
+
+constexpr int kEdgesPerThread = 8;
+
+// Validation + in-degree histogram of the non-self-loop half-arcs.
+__global__ void k_edges(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                        const int32_t* __restrict__ cap, int64_t n, int64_t m, int* indeg, Ctrl* ctrl,
+                        int count_in) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i0 = t * kEdgesPerThread;
+  int loops = 0;
+  if (i0 < m) {
+    int64_t u = row_of(ro, n, i0);
+    int64_t i1 = i0 + kEdgesPerThread < m ? i0 + kEdgesPerThread : m;
+    for (int64_t i = i0; i < i1; ++i) {
+      while (__ldg(ro + u + 1) <= i) ++u;
+      int v = col[i], c = cap[i];
+      if (v < 0 || v >= n || c < 0) {
+        atomicMin((unsigned long long*)&ctrl->bad_edge, (unsigned long long)i);
+        continue;
+      }
+      if (v == u) { ++loops; continue; }
+      if (count_in) atomicAdd(indeg + v, 1);
+    }
+  }
+  loops = warp_sum(loops);
+  if (lane_id() == 0 && loops) atomicAdd(&ctrl->selfloops, loops);
+}
+
+__global__ void k_add(int* a, const int* __restrict__ b, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] += b[i];
+}
+
+__global__ void k_maxlen(const int* __restrict__ deg, int64_t n, Ctrl* ctrl) {
+  int mx = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, deg[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+  if (lane_id() == 0) atomicMax(&ctrl->maxlen, mx);
+}
+
+// BCSR scatter: out half-arc of edge i at soff[u] + (i - ro[u]) with key (v, c);
+// in half-arc at soff[v] + outdeg(v) + cursor[v]++ with key (u, 0).
+__global__ void k_scatter_bcsr(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                               const int32_t* __restrict__ cap, int64_t n, int64_t m,
+                               const int* __restrict__ soff, int* cursor, uint64_t* keys) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i0 = t * kEdgesPerThread;
+  if (i0 >= m) return;
+  int64_t u = row_of(ro, n, i0);
+  int64_t i1 = i0 + kEdgesPerThread < m ? i0 + kEdgesPerThread : m;
+  for (int64_t i = i0; i < i1; ++i) {
+    while (__ldg(ro + u + 1) <= i) ++u;
+    int v = col[i], c = cap[i];
+    int64_t pos = soff[u] + (i - ro[u]);
+    if (v == u) { keys[pos] = kSent; continue; }
+    keys[pos] = ((uint64_t)(uint32_t)v << 32) | (uint32_t)c;
+    int vo = (int)(__ldg(ro + v + 1) - __ldg(ro + v));
+    int q = soff[v] + vo + atomicAdd(cursor + v, 1);
+    keys[q] = ((uint64_t)(uint32_t)u << 32);
+  }
+}
+
+// RCSR forward keys: the input CSR order is already the segment layout.
+__global__ void k_keys_fwd(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                           const int32_t* __restrict__ cap, int64_t n, int64_t m, uint64_t* keys) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i0 = t * kEdgesPerThread;
+  if (i0 >= m) return;
+  int64_t u = row_of(ro, n, i0);
+  int64_t i1 = i0 + kEdgesPerThread < m ? i0 + kEdgesPerThread : m;
+  for (int64_t i = i0; i < i1; ++i) {
+    while (__ldg(ro + u + 1) <= i) ++u;
+    int v = col[i];
+    keys[i] = (v == u) ? kSent : (((uint64_t)(uint32_t)v << 32) | (uint32_t)cap[i]);
+  }
+}
+
+__global__ void k_ro_to_i32(const int64_t* __restrict__ ro, int64_t n, int* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int)ro[i];
+}
+
+// flags[soff[x]] = 1 for non-empty segments (row starts).
+__global__ void k_rowstarts(const int* __restrict__ soff, int64_t n, int* flags) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+    if (soff[x] < soff[x + 1]) flags[soff[x]] = 1;
+}
+
+// head(j) = key is real and (j starts its row or its column differs from j-1)
+__global__ void k_heads(const uint64_t* __restrict__ keys, int64_t H, int* flags) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < H; j += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[j];
+    int f;
+    if (k == kSent) f = 0;
+    else if (flags[j]) f = 1;
+    else f = (uint32_t)(k >> 32) != (uint32_t)(keys[j - 1] >> 32);
+    flags[j] = f;
+  }
+}
+
+// new offsets: off[x] = scan[soff[x]]
+__global__ void k_newoff(const int* __restrict__ soff, const int* __restrict__ scan, int64_t n, int* off) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x <= n; x += (int64_t)gridDim.x * blockDim.x)
+    off[x] = scan[soff[x]];
+}
+
+// Merge each run of equal columns into one slot: cf = sum of capacities
+// (parallel edges summed).  Overflow beyond INT32_MAX is reported.
+__global__ void k_merge_write(const uint64_t* __restrict__ keys, int64_t H, const int* __restrict__ scan,
+                              int2* arc, int* cap0, Ctrl* ctrl) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < H; j += (int64_t)gridDim.x * blockDim.x) {
+    int slot = scan[j];
+    if (scan[j + 1] == slot) continue;  // not a head
+    uint64_t k = keys[j];
+    uint32_t c = (uint32_t)(k >> 32);
+    long long sum = (long long)(uint32_t)(k & 0xffffffffu);
+    for (int64_t q = j + 1; q < H; ++q) {
+      if (scan[q + 1] != scan[q]) break;  // next head
+      uint64_t kq = keys[q];
+      if (kq == kSent) break;
+      sum += (long long)(uint32_t)(kq & 0xffffffffu);
+    }
+    if (sum > INT_MAX) { atomicExch(&ctrl->overflow, 1); sum = INT_MAX; }
+    arc[slot] = make_int2((int)c, (int)sum);
+    if (cap0) cap0[slot] = (int)sum;
+  }
+}
+
+// mate[p] = position of the owner u inside seg(col[p]) — binary search on the
+// sorted segment, once per slot.  8 consecutive slots per thread
+// share one owner search.
+__global__ void k_mate(const int* __restrict__ off, const int2* __restrict__ arc, int n, int M, int* mate,
+                       Ctrl* ctrl) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t p0 = t * kEdgesPerThread;
+  if (p0 >= M) return;
+  int u = row_of32(off, n, (int)p0);
+  int p1 = (int)(p0 + kEdgesPerThread < (int64_t)M ? p0 + kEdgesPerThread : (int64_t)M);
+  for (int p = (int)p0; p < p1; ++p) {
+    while (__ldg(off + u + 1) <= p) ++u;
+    int v = arc[p].x;
+    int lo = __ldg(off + v), hi = __ldg(off + v + 1);
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (arc[mid].x < u) lo = mid + 1; else hi = mid;
+    }
+    if (lo >= __ldg(off + v + 1) || arc[lo].x != u) { atomicExch(&ctrl->overflow, 2); lo = p; }
+    mate[p] = lo;
+  }
+}
+
+// RCSR reverse in-degree over forward arcs
+__global__ void k_rdeg(const int2* __restrict__ farc, int Mf, int* rdeg) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < Mf; p += gridDim.x * blockDim.x)
+    atomicAdd(rdeg + farc[p].x, 1);
+}
+
+// RCSR reverse scatter: forward arc p = (u -> v) lands in v's reverse segment
+// with key (u, p); u distinct per segment after the merge, so keys are unique.
+__global__ void k_scatter_rev(const int* __restrict__ foff, const int2* __restrict__ farc, int n, int Mf,
+                              const int* __restrict__ roff, int* cursor, uint64_t* keys) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t p0 = t * kEdgesPerThread;
+  if (p0 >= Mf) return;
+  int u = row_of32(foff, n, (int)p0);
+  int p1 = (int)(p0 + kEdgesPerThread < (int64_t)Mf ? p0 + kEdgesPerThread : (int64_t)Mf);
+  for (int p = (int)p0; p < p1; ++p) {
+    while (__ldg(foff + u + 1) <= p) ++u;
+    int v = farc[p].x;
+    int q = roff[v] + atomicAdd(cursor + v, 1);
+    keys[q] = ((uint64_t)(uint32_t)u << 32) | (uint32_t)p;
+  }
+}
+
+__global__ void k_write_rarc(const uint64_t* __restrict__ keys, int Mf, int2* rarc, int* bcf) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Mf; q += gridDim.x * blockDim.x) {
+    uint64_t k = keys[q];
+    rarc[q] = make_int2((int)(k >> 32), (int)(k & 0xffffffffu));
+    bcf[q] = 0;   // backward cf of forward arc q (indexed by forward arc)
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static unsigned grid_for(int64_t items, int threads, int num_sms, int per_sm = 16) {
+  int64_t b = (items + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms * per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+static unsigned grid_exact(int64_t items, int threads) {
+  int64_t b = (items + threads - 1) / threads;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+// Phase 1 of the build: validation and segment lengths.  Leaves seg lengths in
+// deg[] and fills ctrl->{bad_edge, bad_rows, selfloops, maxlen}.
+void build_validate(const BuildArgs& a, cudaStream_t st) {
+  const int T = 256;
+  k_rows<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.ro, a.n, a.m, a.deg, a.ctrl);
+  int64_t threads = (a.m + kEdgesPerThread - 1) / kEdgesPerThread;
+  if (a.m > 0)
+    k_edges<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, a.n, a.m, a.deg, a.ctrl,
+                                                   a.layout == 0 ? 1 : 0);
+  k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl);
+}
+
+// Phase 2 (after the host checked the validation record): sort, merge, mate.
+void build_bcsr(const BuildArgs& a, cudaStream_t st) {
+  const int T = 256;
+  const int64_t n = a.n, m = a.m;
+  // soff = exclusive scan of segment lengths
+  cudaMemcpyAsync(a.soff, a.deg, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
+  exclusive_scan(a.soff, n, a.scan_part, st);
+  const int64_t H = a.H;  // = soff[n], known on host
+  cudaMemsetAsync(a.cursor, 0, sizeof(int) * n, st);
+  int64_t threads = (m + kEdgesPerThread - 1) / kEdgesPerThread;
+  if (m > 0)
+    k_scatter_bcsr<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, a.soff, a.cursor, a.keys);
+  segmented_sort(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.ctrl, (int2*)a.arc, a.q0, a.num_sms, st);
+  int* flags = (int*)a.tmp;
+  cudaMemsetAsync(flags, 0, sizeof(int) * (H + 1), st);
+  k_rowstarts<<<grid_for(n, T, a.num_sms), T, 0, st>>>(a.soff, n, flags);
+  if (H > 0) k_heads<<<grid_for(H, T, a.num_sms, 32), T, 0, st>>>(a.keys, H, flags);
+  exclusive_scan(flags, H, a.scan_part, st);
+  k_newoff<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.soff, flags, n, a.off);
+  if (H > 0) k_merge_write<<<grid_for(H, T, a.num_sms, 32), T, 0, st>>>(a.keys, H, flags, a.arc, a.cap0, a.ctrl);
+  cudaMemcpyAsync(&a.ctrl->M, flags + H, sizeof(int), cudaMemcpyDeviceToDevice, st);
+}
+
+void build_bcsr_mate(const BuildArgs& a, int M, cudaStream_t st) {
+  const int T = 256;
+  int64_t threads = ((int64_t)M + kEdgesPerThread - 1) / kEdgesPerThread;
+  if (M > 0) k_mate<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.arc, (int)a.n, M, a.mate, a.ctrl);
+}
+
+void build_rcsr_forward(const BuildArgs& a, cudaStream_t st) {
+  const int T = 256;
+  const int64_t n = a.n, m = a.m;
+  k_ro_to_i32<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.ro, n, a.soff);
+  int64_t threads = (m + kEdgesPerThread - 1) / kEdgesPerThread;
+  if (m > 0) k_keys_fwd<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, a.keys);
+  segmented_sort(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.ctrl, (int2*)a.arc, a.q0, a.num_sms, st);
+  int* flags = (int*)a.tmp;
+  cudaMemsetAsync(flags, 0, sizeof(int) * (m + 1), st);
+  k_rowstarts<<<grid_for(n, T, a.num_sms), T, 0, st>>>(a.soff, n, flags);
+  if (m > 0) k_heads<<<grid_for(m, T, a.num_sms, 32), T, 0, st>>>(a.keys, m, flags);
+  exclusive_scan(flags, m, a.scan_part, st);
+  k_newoff<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.soff, flags, n, a.off);
+  if (m > 0) k_merge_write<<<grid_for(m, T, a.num_sms, 32), T, 0, st>>>(a.keys, m, flags, a.arc, a.cap0, a.ctrl);
+  cudaMemcpyAsync(&a.ctrl->M, flags + m, sizeof(int), cudaMemcpyDeviceToDevice, st);
+}
+
+// Reverse CSR over the Mf merged forward arcs; needs the max reverse segment
+// length (host-known after a sync) for the sort.
+void build_rcsr_reverse_counts(const BuildArgs& a, int Mf, cudaStream_t st) {
+  const int T = 256;
+  cudaMemsetAsync(a.deg, 0, sizeof(int) * a.n, st);
+  if (Mf > 0) k_rdeg<<<grid_for(Mf, T, a.num_sms, 32), T, 0, st>>>(a.arc, Mf, a.deg);
+  cudaMemsetAsync(&a.ctrl->maxlen, 0, sizeof(int), st);
+  k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl);
+  cudaMemcpyAsync(a.roff, a.deg, sizeof(int) * a.n, cudaMemcpyDeviceToDevice, st);
+  exclusive_scan(a.roff, a.n, a.scan_part, st);
+}
+
+void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st) {
+  const int T = 256;
+  cudaMemsetAsync(a.cursor, 0, sizeof(int) * a.n, st);
+  int64_t threads = ((int64_t)Mf + kEdgesPerThread - 1) / kEdgesPerThread;
+  if (Mf > 0)
+    k_scatter_rev<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.arc, (int)a.n, Mf, a.roff, a.cursor, a.keys);
+  segmented_sort(a.keys, a.tmp, a.roff, (int)a.n, maxlen, a.ctrl, a.rarc, a.q0, a.num_sms, st);
+  if (Mf > 0) k_write_rarc<<<grid_for(Mf, T, a.num_sms, 32), T, 0, st>>>(a.keys, Mf, a.rarc, a.bcf);
+}
+
+}  // namespace wbpr

@@ -1,0 +1,105 @@
+// common.cuh — device helpers shared by the WBPR sm_100a kernels.
+//
+// Memory-model notes (B200, sm_100a):
+//  * The persistent solve kernel crosses grid barriers; L1 is not coherent across
+//    SMs, so every MUTABLE array (cf, e, h, queues, counters) is read with
+//    ld.global.cg / ld.relaxed.gpu (served by L2), never through L1.
+//  * Immutable arrays (offsets, columns in a separate array, mate, terminal flags)
+//    go through the read-only path (ld.global.nc).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define WBPR_HOSTDEV __host__ __device__ __forceinline__
+#define WBPR_DEV __device__ __forceinline__
+
+namespace wbpr {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int kWarp = 32;
+
+// ----------------------------------------------------------------- loads / stores
+WBPR_DEV int ld_cg(const int* p) { int v; asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(p)); return v; }
+WBPR_DEV unsigned ld_cg(const unsigned* p) { unsigned v; asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(v) : "l"(p)); return v; }
+WBPR_DEV long long ld_cg(const long long* p) { long long v; asm volatile("ld.global.cg.s64 %0, [%1];" : "=l"(v) : "l"(p)); return v; }
+WBPR_DEV unsigned long long ld_cg(const unsigned long long* p) { unsigned long long v; asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(v) : "l"(p)); return v; }
+WBPR_DEV int2 ld_cg(const int2* p) { int2 v; asm volatile("ld.global.cg.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p)); return v; }
+WBPR_DEV int4 ld_cg(const int4* p) { int4 v; asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p)); return v; }
+WBPR_DEV void st_cg(int* p, int v) { asm volatile("st.global.cg.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory"); }
+WBPR_DEV void st_cg(long long* p, long long v) { asm volatile("st.global.cg.s64 [%0], %1;" :: "l"(p), "l"(v) : "memory"); }
+
+WBPR_DEV unsigned ld_acquire(const unsigned* p) {
+  unsigned v; asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
+}
+WBPR_DEV int ld_volatile(const int* p) { int v; asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p)); return v; }
+
+template <typename T> WBPR_DEV T ld_nc(const T* p) { return __ldg(p); }
+
+WBPR_DEV unsigned long long globaltimer() {
+  unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
+}
+
+// ----------------------------------------------------------------- warp helpers
+WBPR_DEV int lane_id() { return threadIdx.x & 31; }
+WBPR_DEV int warp_id() { return threadIdx.x >> 5; }
+
+template <typename T> WBPR_DEV T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// ----------------------------------------------------------------- block reductions
+template <typename T> __device__ T block_sum(T v, T* smem /* >= 32 */) {
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane_id() == 0) smem[warp_id()] = v;
+  __syncthreads();
+  T r = 0;
+  if (warp_id() == 0) {
+    r = (lane_id() < (int)(blockDim.x >> 5)) ? smem[lane_id()] : T(0);
+    r = warp_sum(r);
+  }
+  return r;  // valid in thread 0
+}
+
+// ----------------------------------------------------------------- grid barrier
+// Software barrier for a cooperative (co-resident) grid.  The last arriving CTA
+// resets the count and bumps the generation.  Waiters back off with nanosleep and
+// give up after the watchdog deadline, setting *abort (never hangs the device).
+struct GridBarrier {
+  unsigned count;
+  unsigned gen;
+};
+
+WBPR_DEV bool grid_sync(GridBarrier* b, unsigned nblocks, unsigned& gen, int* abort,
+                        unsigned long long deadline) {
+  __syncthreads();
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) {
+    int ab = 0;
+    __threadfence();
+    unsigned arrived = atomicAdd(&b->count, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(&b->count, 0u);
+      __threadfence();
+      atomicAdd(&b->gen, 1u);
+    } else {
+      unsigned ns = 8;
+      while (ld_acquire(&b->gen) == gen) {
+        if (ld_volatile(abort)) { ab = 1; break; }
+        if (globaltimer() > deadline) { atomicExch(abort, 1); ab = 1; break; }
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
+    }
+    __threadfence();
+    if (!ab) ab = ld_volatile(abort);
+    s_abort = ab;
+  }
+  gen++;
+  __syncthreads();
+  return s_abort == 0;
+}
+
+}  // namespace wbpr

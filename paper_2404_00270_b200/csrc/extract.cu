@@ -1,0 +1,79 @@
+// extract.cu — A8: results after the final exact global relabel.
+//   flow_i   = e(t_i)                         (Alg. 1 output)
+//   bitmap   bit v = [h(v) >= |V|]            (after the final exact GR this is the
+//                                             set that cannot reach a sink = S*)
+//   cutcap_i = sum of c(u,v) over INPUT edges with u in S*, v not in S*, per instance
+//              (the device certificate: must equal flow_i by max-flow/min-cut duality,
+//              P:120-127)
+#include "internal.h"
+#include "kernels.h"
+
+namespace wbpr {
+
+__global__ void k_bitmap(const int* __restrict__ h, int n, int N, uint32_t* bitmap) {
+  int nwords = (n + 31) >> 5;
+  for (int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < nwords * 32;
+       base += gridDim.x * blockDim.x) {
+    int v = base + lane_id();
+    bool in_s = v < n && ld_cg(h + v) >= N;
+    unsigned b = __ballot_sync(FULL, in_s);
+    if (lane_id() == 0) bitmap[base >> 5] = b;
+  }
+}
+
+constexpr int kCutEdges = 8;
+
+__global__ void k_cutcap(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                         const int32_t* __restrict__ cap, int64_t n, int64_t m, const int* __restrict__ h, int N,
+                         const int64_t* __restrict__ vbase, int k, long long* cut) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i0 = t * kCutEdges;
+  if (i0 >= m) return;
+  int64_t lo = 0, hi = n;
+  while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (__ldg(ro + mid) <= i0) lo = mid; else hi = mid; }
+  int64_t u = lo;
+  int inst = 0;
+  { int a = 0, b = k; while (b - a > 1) { int mid = (a + b) >> 1; if (__ldg(vbase + mid) <= u) a = mid; else b = mid; } inst = a; }
+  long long acc = 0;
+  int64_t i1 = i0 + kCutEdges < m ? i0 + kCutEdges : m;
+  int hu = ld_cg(h + u);
+  for (int64_t i = i0; i < i1; ++i) {
+    while (__ldg(ro + u + 1) <= i) {
+      ++u;
+      hu = ld_cg(h + u);
+      if (u >= __ldg(vbase + inst + 1)) {
+        if (acc) atomicAdd((unsigned long long*)(cut + inst), (unsigned long long)acc);
+        acc = 0;
+        while (u >= __ldg(vbase + inst + 1)) ++inst;
+      }
+    }
+    int v = col[i];
+    if (hu >= N && ld_cg(h + v) < N) acc += cap[i];
+  }
+  if (acc) atomicAdd((unsigned long long*)(cut + inst), (unsigned long long)acc);
+}
+
+__global__ void k_flows(const long long* __restrict__ e, const long long* __restrict__ snk, int k, long long* flow) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
+    flow[i] = ld_cg(e + snk[i]);
+}
+
+void extract_results(const SolveParams& p, const int64_t* ro, const int32_t* col, const int32_t* cap,
+                     int64_t m, uint32_t* bitmap, const int64_t* vbase, int k, long long* inst_flow,
+                     long long* inst_cut, int num_sms, cudaStream_t st) {
+  const int T = 256;
+  if (bitmap) {
+    int64_t words = (p.n + 31) / 32;
+    int64_t blocks = (words * 32 + T - 1) / T;
+    if (blocks > num_sms * 16) blocks = num_sms * 16;
+    k_bitmap<<<(unsigned)blocks, T, 0, st>>>(p.h, p.n, p.n, bitmap);
+  }
+  cudaMemsetAsync(inst_cut, 0, sizeof(long long) * k, st);
+  if (m > 0) {
+    int64_t threads = (m + kCutEdges - 1) / kCutEdges;
+    k_cutcap<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(ro, col, cap, p.n, m, p.h, p.n, vbase, k, inst_cut);
+  }
+  k_flows<<<(k + T - 1) / T, T, 0, st>>>(p.e, p.snk, k, inst_flow);
+}
+
+}  // namespace wbpr

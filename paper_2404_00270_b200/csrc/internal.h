@@ -1,0 +1,142 @@
+// internal.h — workspace layout and device control block shared by the host
+// orchestration (api.cu) and the kernels.  Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace wbpr {
+
+constexpr int kChunk = 1024;       // slots per warp task; vertices with more slots are "huge"
+constexpr int kSortTile = 4096;    // CTA shared-memory sort tile (64-bit keys)
+constexpr int kScanTile = 4096;    // elements per scan tile
+constexpr int kMaxInst = 1 << 20;  // batch instances
+
+// Vertex terminal flags (term[v])
+constexpr uint8_t kSource = 1;
+constexpr uint8_t kSink = 2;
+
+// Per-phase counters, triple-buffered by phase parity (see solve.cu).
+struct Ring {
+  unsigned long long work;  // relabel work (slots scanned by relabels)
+  int qn;                   // appended normal queue entries
+  int hn;                   // appended huge vertices
+  int hc;                   // appended huge chunk tasks
+  int pad[3];
+};
+
+// Huge-vertex record for one round: chunk tasks fold their partial minima into
+// `best` and the last chunk (done == nchunks) performs the push or relabel.
+struct HugeRec {
+  unsigned long long best;  // (h << 32) | slot
+  int u;
+  int nchunks;
+  int done;
+  int pad;
+};
+
+enum StatIdx {
+  ST_ROUNDS = 0, ST_GRS, ST_BFS_LEVELS, ST_PUSHES, ST_RELABELS, ST_ARCS, ST_BFS_ARCS,
+  ST_CAND, ST_AVQ, ST_GAPLIFT, ST_COUNT = 16
+};
+
+enum DevStatus { DS_OK = 0, DS_NOTCONVERGED = 1, DS_TIMEOUT = 2, DS_INTERNAL = 3 };
+
+// Device control block at the start of the workspace.
+struct Ctrl {
+  GridBarrier bar;
+  int abort;
+  int status;
+  Ring ring[3];
+  long long excess_total;
+  long long stats[ST_COUNT];
+  // build info
+  long long bad_edge;     // first offending edge index (min), LLONG_MAX if none
+  int bad_rows;           // row offsets malformed
+  int overflow;           // merged capacity > INT32_MAX
+  int maxlen;             // longest build segment
+  int M;                  // residual slots (BCSR) / forward arcs (RCSR)
+  int Mr;                 // RCSR reverse entries
+  int selfloops;
+  int hub_chunks;         // build scratch counter
+  int sort_items;         // build scratch counter
+  int pad0[6];
+  long long gap_level;    // online gap: lowest empty level seen this round (A6)
+};
+
+// Byte offsets of every region of a workspace (all 256-B aligned).
+struct Layout {
+  int64_t n, m, k, H;       // H = 2m half-arcs (BCSR) ; RCSR uses m + m
+  int32_t layout;
+  size_t ctrl, inst_s, inst_t, inst_flow, inst_cut, vbase;
+  size_t in_row, in_col, in_cap;           // staging copy of a host CSR
+  size_t h, e, term, deact, deg, cursor, off, soff, roff, rsoff;
+  size_t q0, q1, hq0, hq1, hc0, hc1, hist;
+  size_t scan_part;
+  size_t regA, regB, regC;                 // build / residual regions
+  size_t bcap0;                            // offset inside regB of cap0
+  size_t total;
+};
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout) {
+  Layout L{};
+  L.n = n; L.m = m; L.k = k; L.layout = layout;
+  L.H = 2 * m;
+  const int64_t H = L.H;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t r = o; o = align_up(o + bytes); return r; };
+  L.ctrl = take(sizeof(Ctrl));
+  L.inst_s = take(8 * k); L.inst_t = take(8 * k); L.inst_flow = take(8 * k); L.inst_cut = take(8 * k);
+  L.vbase = take(8 * (k + 1));
+  L.in_row = take(8 * (n + 1)); L.in_col = take(4 * m + 4); L.in_cap = take(4 * m + 4);
+  L.h = take(4 * n); L.e = take(8 * n); L.term = take(n); L.deact = take(n);
+  L.deg = take(4 * n + 4); L.cursor = take(4 * n + 4);
+  L.off = take(4 * (n + 1)); L.soff = take(4 * (n + 1)); L.roff = take(4 * (n + 1)); L.rsoff = take(4 * (n + 1));
+  L.q0 = take(4 * n + 4); L.q1 = take(4 * n + 4);
+  int64_t hub = H / kChunk + 64;
+  L.hq0 = take(sizeof(HugeRec) * hub); L.hq1 = take(sizeof(HugeRec) * hub);
+  L.hc0 = take(8 * (2 * hub + 64)); L.hc1 = take(8 * (2 * hub + 64));
+  L.hist = take(4 * (n + 2));
+  L.scan_part = take(4 * ((H + 2 + n) / kScanTile + 64));
+  L.regA = take(8 * H + 8);
+  L.regB = take(8 * H + 1024);
+  L.bcap0 = align_up(4 * H + 260);
+  L.regC = take(8 * H + 8);
+  L.total = o;
+  return L;
+}
+
+// Launch parameters of the persistent solve kernel.
+struct SolveParams {
+  Ctrl* ctrl;
+  int n;                 // vertices (union)
+  int k;                 // instances
+  int layout;
+  int M, Mf;             // slots (BCSR) / forward arcs (RCSR)
+  const int* off;        // BCSR offsets or RCSR forward offsets
+  int2* arc;             // {col, cf}
+  const int* mate;       // BCSR
+  const int* roff;       // RCSR reverse offsets
+  const int2* rarc;      // RCSR {col, fidx}
+  int* bcf;              // RCSR backward cf
+  int* h;
+  long long* e;
+  const uint8_t* term;
+  uint8_t* deact;
+  int* q[2];
+  HugeRec* hq[2];
+  int2* hc[2];
+  int* hist;
+  const long long* src; // sources [k]
+  const long long* snk; // sinks [k]
+  long long max_rounds;
+  unsigned long long gr_threshold;
+  int gap_mode;
+  unsigned long long deadline_ns_rel;
+};
+
+}  // namespace wbpr

@@ -1,0 +1,65 @@
+// kernels.h — host-callable launch wrappers of the WBPR kernels (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace wbpr {
+
+void exclusive_scan(int* a, int64_t N, int* part, cudaStream_t st);
+
+void segmented_sort(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl,
+                    int2* items, int* big, int num_sms, cudaStream_t st);
+
+struct BuildArgs {
+  int64_t n, m, H;
+  int32_t layout;
+  int num_sms;
+  const int64_t* ro;
+  const int32_t* col;
+  const int32_t* cap;
+  Ctrl* ctrl;
+  int* deg;
+  int* cursor;
+  int* soff;
+  int* off;
+  int* roff;
+  int* scan_part;
+  int* q0;
+  uint64_t* keys;  // region A
+  uint64_t* tmp;   // region B
+  int2* arc;       // region C
+  int* mate;       // region B (after the merge)
+  int* cap0;       // region B + bcap0
+  int2* rarc;      // region C + 8m (RCSR)
+  int* bcf;        // region B (RCSR)
+  int maxlen;
+};
+
+void build_validate(const BuildArgs& a, cudaStream_t st);
+void build_bcsr(const BuildArgs& a, cudaStream_t st);
+void build_bcsr_mate(const BuildArgs& a, int M, cudaStream_t st);
+void build_rcsr_forward(const BuildArgs& a, cudaStream_t st);
+void build_rcsr_reverse_counts(const BuildArgs& a, int Mf, cudaStream_t st);
+void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st);
+
+// solve.cu
+int solve_max_blocks_per_sm(int layout, int threads);
+cudaError_t launch_solve(const SolveParams& p, int blocks, int threads, cudaStream_t st);
+constexpr int kSolveThreads = 512;
+
+// extract.cu
+void extract_results(const SolveParams& p, const int64_t* ro, const int32_t* col, const int32_t* cap,
+                     int64_t m, uint32_t* bitmap, const int64_t* vbase, int k, long long* inst_flow,
+                     long long* inst_cut, int num_sms, cudaStream_t st);
+
+// bipartite.cu
+void bip_validate(int64_t nL, int64_t nR, int64_t E, const int32_t* l, const int32_t* r, int* deg, int* cursor,
+                  Ctrl* ctrl, int num_sms, cudaStream_t st);
+void bip_build(int64_t nL, int64_t nR, int64_t E, const int32_t* l, const int32_t* r, int64_t* ro, int32_t* col,
+               int32_t* cap, int* deg, int* cursor, int* scan_part, int num_sms, cudaStream_t st);
+void bip_extract(const SolveParams& p, int64_t nL, int64_t nR, int32_t* match_of_left, int num_sms,
+                 cudaStream_t st);
+
+}  // namespace wbpr

@@ -1,0 +1,168 @@
+// segsort.cu — hand-written segmented sort of 64-bit keys for residual
+// construction (A1).  BCSR needs every vertex segment sorted by column (PAPER.md
+// §3.2, "sort the column list in ascending order by vertex ID") so that
+// duplicate columns become adjacent (merge) and the reverse arc can be located
+// by binary search once, into mate[].
+//
+// Segment classes (lengths from 1 to ~1.6e5 at R-MAT scale 22):
+//   len <= 32        one warp per segment, rank sort in registers (32 shuffles)
+//   32 < len <= 4096 one CTA per segment, bitonic sort in shared memory
+//   len > 4096       4096-key chunks sorted as above, then log2(len/4096)
+//                    merge passes (merge-path co-rank, 8 outputs per thread),
+//                    ping-ponging between keys and tmp.
+#include "internal.h"
+#include "kernels.h"
+
+namespace wbpr {
+
+constexpr int kTileThreads = 512;
+
+__global__ void __launch_bounds__(256) k_sort_warp(uint64_t* keys, const int* __restrict__ off, int nseg) {
+  int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = lane_id();
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int sgi = wg; sgi < nseg; sgi += nw) {
+    int beg = off[sgi], len = off[sgi + 1] - beg;
+    if (len < 2 || len > 32) continue;
+    uint64_t k = lane < len ? keys[beg + lane] : ~0ull;
+    int rank = 0;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      uint64_t o = __shfl_sync(FULL, k, j);
+      rank += (o < k) || (o == k && j < lane);
+    }
+    __syncwarp();
+    if (lane < len) keys[beg + rank] = k;
+  }
+}
+
+// Enumerate CTA sort items: segments with 32 < len <= tile as one item, longer
+// segments as ceil(len/tile) chunk items; longer segments also go to `big`.
+__global__ void k_sort_items(const int* __restrict__ off, int nseg, int2* items, int* big, Ctrl* ctrl) {
+  for (int sgi = blockIdx.x * blockDim.x + threadIdx.x; sgi < nseg; sgi += gridDim.x * blockDim.x) {
+    int beg = off[sgi], len = off[sgi + 1] - beg;
+    if (len <= 32) continue;
+    int nit = (len + kSortTile - 1) / kSortTile;
+    int idx = atomicAdd(&ctrl->sort_items, nit);
+    for (int c = 0; c < nit; ++c) {
+      int s = beg + c * kSortTile;
+      int l = min(kSortTile, beg + len - s);
+      items[idx + c] = make_int2(s, l);
+    }
+    if (nit > 1) big[atomicAdd(&ctrl->hub_chunks, 1)] = sgi;
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_sort_tile(uint64_t* keys, const int2* __restrict__ items,
+                                                             const Ctrl* ctrl) {
+  __shared__ uint64_t s[kSortTile];
+  int nitems = ctrl->sort_items;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    int2 item = items[it];
+    int beg = item.x, len = item.y;
+    int P = 64;
+    while (P < len) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < len ? keys[beg + i] : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < P; i += blockDim.x) {
+          int ixj = i ^ j;
+          if (ixj > i) {
+            uint64_t a = s[i], b = s[ixj];
+            bool up = (i & k) == 0;
+            if ((a > b) == up) { s[i] = b; s[ixj] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) keys[beg + i] = s[i];
+    __syncthreads();
+  }
+}
+
+// Smallest i in [max(0,k-lb), min(k,la)] with A[i] > B[k-i-1] (A wins ties): the
+// number of outputs among the first k that come from A.
+__device__ __forceinline__ int co_rank(int k, const uint64_t* A, int la, const uint64_t* B, int lb) {
+  int lo = k - lb > 0 ? k - lb : 0, hi = k < la ? k : la;
+  while (lo < hi) {
+    int i = (lo + hi) >> 1;          // candidate: i from A, k-i from B
+    // too few from A if A[i] <= B[k-i-1]
+    if (A[i] <= B[k - i - 1]) lo = i + 1; else hi = i;
+  }
+  return lo;
+}
+
+// One merge pass of width w over every big segment (one CTA per segment).
+__global__ void __launch_bounds__(256) k_merge_pass(const uint64_t* __restrict__ src, uint64_t* dst,
+                                                    const int* __restrict__ off, const int* __restrict__ big,
+                                                    const Ctrl* ctrl, int w) {
+  int nbig = ctrl->hub_chunks;
+  for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    int sgi = big[bi];
+    int beg = off[sgi], len = off[sgi + 1] - beg;
+    int ntask = (len + 7) >> 3;
+    for (int tk = threadIdx.x; tk < ntask; tk += blockDim.x) {
+      int kk = tk << 3;                       // local output index
+      int pair0 = kk / (2 * w) * (2 * w);     // start of the pair of runs
+      int la = min(w, len - pair0);
+      int lb = min(w, len - pair0 - la);
+      if (lb < 0) lb = 0;
+      const uint64_t* A = src + beg + pair0;
+      const uint64_t* B = A + la;
+      int k = kk - pair0;
+      int i = co_rank(k, A, la, B, lb);
+      int j = k - i;
+      int outn = min(8, la + lb - k);
+      uint64_t* O = dst + beg + kk;
+      for (int q = 0; q < outn; ++q) {
+        bool takeA = j >= lb || (i < la && A[i] <= B[j]);
+        O[q] = takeA ? A[i++] : B[j++];
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_copy_big(const uint64_t* __restrict__ src, uint64_t* dst,
+                                                  const int* __restrict__ off, const int* __restrict__ big,
+                                                  const Ctrl* ctrl) {
+  int nbig = ctrl->hub_chunks;
+  for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+    int sgi = big[bi];
+    int beg = off[sgi], len = off[sgi + 1] - beg;
+    for (int i = threadIdx.x; i < len; i += blockDim.x) dst[beg + i] = src[beg + i];
+  }
+}
+
+void segmented_sort(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl,
+                    int2* items, int* big, int num_sms, cudaStream_t st) {
+  if (nseg <= 0 || maxlen < 2) return;
+  cudaMemsetAsync(&ctrl->sort_items, 0, sizeof(int), st);
+  cudaMemsetAsync(&ctrl->hub_chunks, 0, sizeof(int), st);
+  {
+    int64_t warps = nseg;
+    int64_t blocks = (warps * 32 + 255) / 256;
+    if (blocks > (int64_t)num_sms * 64) blocks = (int64_t)num_sms * 64;
+    k_sort_warp<<<(unsigned)blocks, 256, 0, st>>>(keys, off, nseg);
+  }
+  if (maxlen <= 32) return;
+  {
+    int64_t blocks = (nseg + 255) / 256;
+    if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+    k_sort_items<<<(unsigned)blocks, 256, 0, st>>>(off, nseg, items, big, ctrl);
+  }
+  k_sort_tile<<<num_sms * 4, kTileThreads, 0, st>>>(keys, items, ctrl);
+  if (maxlen <= kSortTile) return;
+  const uint64_t* src = keys;
+  uint64_t* dst = tmp;
+  int passes = 0;
+  for (int w = kSortTile; w < maxlen; w <<= 1) {
+    k_merge_pass<<<num_sms * 8, 256, 0, st>>>(src, dst, off, big, ctrl, w);
+    const uint64_t* t = src; src = dst; dst = const_cast<uint64_t*>(t);
+    ++passes;
+  }
+  if (passes & 1) k_copy_big<<<num_sms * 8, 256, 0, st>>>(tmp, keys, off, big, ctrl);
+}
+
+}  // namespace wbpr

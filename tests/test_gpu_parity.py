@@ -1,0 +1,235 @@
+"""-m gpu parity tests: the CUDA path (through the C-ABI) against the oracle on
+the same seeded inputs.  Integer results must match bit-exactly: flow value,
+min-cut capacity and the canonical cut bitmap (unique); the
+flow assignment (not unique) must pass V1-V7."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from oracle import brute, matching, residual_ref
+from tests.gpu_helpers import assert_parity, bits_to_mask, gpu_solve, to_dev
+
+pytestmark = pytest.mark.gpu
+LAYOUTS = ["bcsr", "rcsr"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2404_00270_b200 as W
+    W.load()
+
+
+# ------------------------------------------------------------------ A1 construction, bit-exact
+def _build(g, layout):
+    import paper_2404_00270_b200 as W
+    ro, col, cap = to_dev(g)
+    return W.build_residual(ro, col, cap, layout=layout)
+
+
+BUILD_CASES = [("tiny", s) for s in range(12)] + [("c1", 1), ("grid", 1), ("rmat", 3), ("hubs", 0)]
+
+
+def _build_graph(kind, seed):
+    if kind == "tiny":
+        return synth.tiny_random(12 + seed, 60 + 10 * seed, 6, seed)
+    if kind == "c1":
+        return synth.shuffle_rows(synth.random_graph(1024, 8192, seed), seed)
+    if kind == "grid":
+        return synth.grid(37, 23, True, seed)
+    if kind == "rmat":
+        return synth.shuffle_rows(synth.rmat(13, 16, seed, "hub20"), seed)
+    if kind == "hubs":
+        # segments of every size class: <=32, <=4096, > 4096 (merge passes), duplicates
+        rng = np.random.default_rng(7)
+        n = 20000
+        src = np.concatenate([np.zeros(9000, np.int64), np.full(5000, 1), rng.integers(0, n, 30000), [5, 5, 5]])
+        dst = np.concatenate([rng.integers(0, n, 9000), rng.integers(0, n, 5000), rng.integers(0, n, 30000), [5, 6, 6]])
+        cap = rng.integers(0, 50, src.shape[0]).astype(np.int32)
+        return synth.shuffle_rows(synth.from_edges(n, src, dst, cap, 0, n - 1), 3)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind,seed", BUILD_CASES)
+def test_build_bcsr_bitexact(kind, seed):
+    g = _build_graph(kind, seed)
+    R, st = _build(g, "bcsr")
+    ref = residual_ref.bcsr(g.n, g.row_off, g.col, g.cap)
+    assert R["M"] == ref["col"].shape[0]
+    assert np.array_equal(R["off"], ref["off"])
+    assert np.array_equal(R["col"], ref["col"])
+    assert np.array_equal(R["cf"], ref["cf0"])
+    assert np.array_equal(R["cap0"], ref["cf0"])
+    assert np.array_equal(R["mate"], ref["mate"])
+    src, dst, _ = g.edges()
+    assert st["self_loops_ignored"] == int((src == dst).sum())
+
+
+@pytest.mark.parametrize("kind,seed", BUILD_CASES)
+def test_build_rcsr_bitexact(kind, seed):
+    g = _build_graph(kind, seed)
+    R, _ = _build(g, "rcsr")
+    ref = residual_ref.rcsr(g.n, g.row_off, g.col, g.cap)
+    assert np.array_equal(R["foff"], ref["foff"])
+    assert np.array_equal(R["fcol"], ref["fcol"])
+    assert np.array_equal(R["fcf"], ref["fcf0"])
+    assert np.array_equal(R["roff"], ref["roff"])
+    assert np.array_equal(R["rcol"], ref["rcol"])
+    assert np.array_equal(R["fidx"], ref["fidx"])
+    assert np.all(R["bcf"] == 0)
+
+
+# ------------------------------------------------------------------ end-to-end parity
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_spec_examples(golden, layout):
+    for ex in golden["maxflow"]:
+        e = np.array(ex["edges"], np.int64).reshape(-1, 3)
+        g = synth.from_edges(ex["n"], e[:, 0], e[:, 1], e[:, 2], ex["s"], ex["t"])
+        F, _ = assert_parity(g, layout)
+        assert F == ex["flow"], ex["citation"]
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("chunk", range(4))
+def test_tiny_random_vs_brute_force(layout, chunk):
+    for seed in range(chunk * 60, chunk * 60 + 60):
+        rng = np.random.default_rng(50_000 + seed)
+        n = int(rng.integers(2, 12))
+        g = synth.tiny_random(n, int(rng.integers(0, 40)), int(rng.integers(1, 9)), seed)
+        F, _ = assert_parity(g, layout)
+        if n <= 10:
+            c, S_max = brute.enum_mincut(g.n, g.row_off, g.col, g.cap, g.s, g.t)
+            assert F == c
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("seed", range(1, 17))
+def test_c1_seeds(layout, seed):
+    assert_parity(synth.random_graph(1024, 8192, seed), layout)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_random_grid(layout):
+    assert_parity(synth.grid(64, 48, True, 5), layout)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("k", [16, 128])
+def test_unit_grid_closed_form(layout, k):
+    F, _ = assert_parity(synth.grid(k, k, False), layout)
+    assert F == k
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("rule", ["paper", "hub20"])
+def test_rmat14(layout, rule):
+    assert_parity(synth.rmat(14, 16, 2, rule), layout)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_huge_vertex_chunks(layout):
+    # a hub with > kChunk slots that must discharge through many rounds
+    rng = np.random.default_rng(11)
+    n = 6000
+    hub = 1
+    src = np.concatenate([[0], np.full(5000, hub), rng.integers(2, n - 1, 20000)])
+    dst = np.concatenate([[hub], rng.integers(2, n - 1, 5000), rng.integers(2, n, 20000)])
+    cap = np.concatenate([[10**6], rng.integers(1, 20, 25000)]).astype(np.int32)
+    g = synth.from_edges(n, src, dst, cap, 0, n - 1)
+    assert_parity(g, layout)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_gr_frequency_and_grid_size_invariance(layout):
+    g = synth.random_graph(3000, 24000, 9, 0, 2999)
+    ref = oracle.maxflow_graph(g, phase2=False)
+    for beta, blocks in ((0.02, 0), (5.0, 0), (0.5, 3), (0.5, 1)):
+        assert_parity(g, layout, ref=ref, validate=False, gr_beta=beta, grid_blocks=blocks)
+
+
+# ------------------------------------------------------------------ host-buffer path (e2e)
+def test_host_buffers():
+    import torch
+    import paper_2404_00270_b200 as W
+    g = synth.random_graph(1024, 8192, 3)
+    ref = oracle.maxflow_graph(g, phase2=False)
+    ro, col, cap = (torch.from_numpy(a).pin_memory() for a in (g.row_off, g.col, g.cap))
+    F, bm, st = W.maxflow(ro, col, cap, g.s, g.t)
+    assert not bm.is_cuda
+    assert F == ref.flow and np.array_equal(bm.numpy().view(np.uint32), ref.bitmap_words())
+
+
+# ------------------------------------------------------------------ bipartite (A9)
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("seed", range(4))
+def test_bipartite(layout, seed):
+    import torch
+    import paper_2404_00270_b200 as W
+    nL, nR = 3000 + 100 * seed, 2500
+    l, r = synth.bipartite_edges(nL, nR, 7000, seed)
+    n, src, dst, cap, s, t = matching.network(nL, nR, l, r)
+    ref = oracle.maxflow_graph(synth.from_edges(n, src, dst, cap, s, t), phase2=False).flow
+    size, match, st = W.bipartite_match(nL, nR, torch.from_numpy(l).cuda(), torch.from_numpy(r).cuda(), layout=layout)
+    assert size == ref
+    matching.check_matching(nL, nR, l, r, match.cpu().numpy(), size)
+
+
+def test_bipartite_spec_examples(golden):
+    import torch
+    import paper_2404_00270_b200 as W
+    for ex in golden["matching"]:
+        l = torch.tensor([e[0] for e in ex["edges"]], dtype=torch.int32, device="cuda")
+        r = torch.tensor([e[1] for e in ex["edges"]], dtype=torch.int32, device="cuda")
+        size, match, _ = W.bipartite_match(ex["nL"], ex["nR"], l, r)
+        assert size == ex["size"], ex["citation"]
+
+
+# ------------------------------------------------------------------ batch (A10)
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_batch_union(layout):
+    import torch
+    import paper_2404_00270_b200 as W
+    parts = [synth.rmat(11, 16, 100 + i, "paper" if i % 2 else "hub20") for i in range(6)]
+    parts += [synth.random_graph(500, 3000, i, 0, 499) for i in range(3)]
+    B = synth.disjoint_union(parts)
+    ro, col, cap = to_dev(B.union)
+    flows, cuts, bm, st = W.maxflow_batch(ro, col, cap, B.vbase, B.s, B.t, layout=layout)
+    mask = bits_to_mask(bm.cpu().numpy().view(np.uint32), B.union.n)
+    for i, g in enumerate(parts):
+        ref = oracle.maxflow_graph(g, phase2=False)
+        assert flows[i] == ref.flow and cuts[i] == ref.flow
+        assert np.array_equal(mask[B.vbase[i]:B.vbase[i + 1]], ref.in_S)
+
+
+# ------------------------------------------------------------------ errors
+def test_errors():
+    import torch
+    import paper_2404_00270_b200 as W
+    g = synth.random_graph(100, 400, 1, 0, 99)
+    ro, col, cap = to_dev(g)
+    with pytest.raises(W.WbprError) as e:
+        W.maxflow(ro, col, cap, 5, 5)
+    assert e.value.name == "WBPR_EINVAL"
+    bad = col.clone(); bad[17] = 100
+    with pytest.raises(W.WbprError) as e:
+        W.maxflow(ro, bad, cap, 0, 99)
+    assert e.value.name == "WBPR_EINVAL"
+    neg = cap.clone(); neg[3] = -1
+    with pytest.raises(W.WbprError) as e:
+        W.maxflow(ro, col, neg, 0, 99)
+    assert e.value.name == "WBPR_EINVAL"
+    h = synth.from_edges(3, [0, 0, 0, 1], [1, 1, 1, 2], [2**30, 2**30, 2**30, 5], 0, 2)
+    ro2, col2, cap2 = to_dev(h)
+    with pytest.raises(W.WbprError) as e:
+        W.maxflow(ro2, col2, cap2, 0, 2)
+    assert e.value.name == "WBPR_EOVERFLOW"
+    import ctypes
+    L = W.load()
+    c = W.wbpr._as_csr(ro, col, cap)
+    small = W.Workspace(1024)
+    rc = L.wbpr_maxflow_solve(ctypes.byref(c), 0, 99, ctypes.byref(W.options()), small.ptr, 1024, None, None,
+                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == -3  # WBPR_ENOMEM
