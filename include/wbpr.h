@@ -82,7 +82,14 @@ typedef struct wbpr_options {
   int64_t max_rounds;    /* push/relabel round cap, 0 -> 10*n + 1000             */
   int32_t grid_blocks;   /* persistent grid size, 0 -> all co-resident CTAs             */
   int32_t timeout_ms;    /* device watchdog, 0 -> 120000                                 */
-  int32_t reserved[6];
+  int32_t push_mode;     /* 0: one push per active vertex per round to its lowest residual
+                            neighbour (Alg. 2); 1: warp-parallel discharge: every
+                            admissible arc (h(v) < h(u)) of the vertex gets a share of e(u) in
+                            the same round (a deviation)                          */
+  float gr_gamma;        /* also GR when the time spent in rounds since the last GR reaches
+                            gr_gamma x the duration of that GR (balances the two; 0 = off);
+                            < 0 -> default 1.0                                               */
+  int32_t reserved[4];
 } wbpr_options;
 
 typedef struct wbpr_stats {
@@ -103,6 +110,7 @@ typedef struct wbpr_stats {
   int64_t excess_total;      /* Excess_total at termination              */
   float build_ms, solve_ms, extract_ms, total_ms; /* CUDA-event times on `stream`       */
   int32_t grid_blocks, block_threads;
+  int64_t kernel_launches;   /* kernels this call launched (all of them this library's own) */
 } wbpr_stats;
 
 /* Fill *opt with the defaults above. */

@@ -1,0 +1,53 @@
+"""Multi-GPU batch plumbing (A10 / §8(e)): instances are partitioned over ranks
+(one process per GPU) and each rank's results travel as fixed 64-B records
+gathered with ONE collective (NCCL all_gather on GPUs, gloo in the CPU tests).
+No collective touches the data path: every rank solves its own instances."""
+from __future__ import annotations
+
+import numpy as np
+
+RECORD_FIELDS = ("instance", "status", "flow", "cut_capacity", "rounds", "global_relabels", "pushes", "relabels")
+
+
+def partition(total: int, world: int, rank: int):
+    """Contiguous block [lo, hi) of instance ids owned by `rank` (sizes differ by <= 1)."""
+    base, extra = divmod(total, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def make_records(ids, flows, cuts, stats=None, status=0) -> np.ndarray:
+    """int64[k, 8] records (64 B each)."""
+    k = len(ids)
+    r = np.zeros((k, len(RECORD_FIELDS)), np.int64)
+    r[:, 0] = ids
+    r[:, 1] = status
+    r[:, 2] = flows
+    r[:, 3] = cuts
+    if stats:
+        r[:, 4] = stats.get("rounds", 0)
+        r[:, 5] = stats.get("global_relabels", 0)
+        r[:, 6] = stats.get("pushes", 0)
+        r[:, 7] = stats.get("relabels", 0)
+    return r
+
+
+def gather_records(local, total: int, world: int, device=None):
+    """All-gather every rank's records; returns int64[total, 8] ordered by instance id.
+    `local` is a torch int64 tensor [k_local, 8] on the collective's device."""
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        out = local
+    else:
+        cap = -(-total // world)   # pad every rank to the same row count
+        buf = torch.full((cap, local.shape[1]), -1, dtype=torch.int64, device=local.device)
+        buf[:local.shape[0]] = local
+        parts = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(parts, buf)
+        out = torch.cat(parts)
+        out = out[out[:, 0] >= 0]
+    out = out[torch.argsort(out[:, 0])]
+    assert out.shape[0] == total and bool((out[:, 0] == torch.arange(total, device=out.device)).all())
+    return out

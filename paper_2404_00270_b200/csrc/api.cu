@@ -72,18 +72,6 @@ __global__ void k_terms(uint8_t* term, const long long* s, const long long* t, i
   }
 }
 
-// batch: every edge must stay inside its instance's vertex range (A10)
-__global__ void k_check_ranges(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n,
-                               const int64_t* __restrict__ vbase, int k, Ctrl* ctrl) {
-  for (int i = blockIdx.x; i < k; i += gridDim.x) {
-    int64_t lo = vbase[i], hi = vbase[i + 1];
-    for (int64_t e = ro[lo] + threadIdx.x; e < ro[hi]; e += blockDim.x) {
-      int v = col[e];
-      if (v < lo || v >= hi) atomicMin((unsigned long long*)&ctrl->bad_edge, (unsigned long long)e);
-    }
-  }
-}
-
 template <typename T> T* at(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
 
 struct Ws {
@@ -104,12 +92,16 @@ wbpr_options resolve(const wbpr_options* o) {
   if (o) r = *o;
   if (!(r.gr_beta > 0.f)) r.gr_beta = 0.5f;
   if (r.timeout_ms <= 0) r.timeout_ms = 120000;
+  if (r.gr_gamma < 0.f) r.gr_gamma = 1.0f;
   return r;
 }
 
-// A1 for one workspace; fills M / Mf.  `ro,col,cap` are device pointers.
+// A1 for one workspace.  BCSR: no host synchronisation after validation (M stays on
+// the device and is read after the solve); RCSR: Mf is read back (the reverse sort
+// needs the longest reverse segment).  `ro,col,cap` are device pointers.
 wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, const int32_t* cap, int layout,
-                           int num_sms, int& M, int& Mf, int64_t& selfloops, int64_t& bad_edge, cudaStream_t st) {
+                           int num_sms, const int64_t* d_vbase, int k, int& Mf, int64_t& selfloops,
+                           int64_t& bad_edge, cudaStream_t st) {
   const Layout& L = W.L;
   BuildArgs a{};
   a.n = L.n; a.m = L.m; a.layout = layout; a.num_sms = num_sms;
@@ -123,6 +115,8 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
   a.cap0 = at<int>(W.base, L.regB + L.bcap0);
   a.rarc = at<int2>(W.base, L.regC + 8 * (size_t)L.m);
   a.bcf = at<int>(W.base, L.regB);
+  a.colv = at<int>(W.base, L.regA);
+  a.vbase = d_vbase; a.k = k;
 
   build_validate(a, st);
   CK(cudaGetLastError());
@@ -133,21 +127,15 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
   bad_edge = c.bad_edge == LLONG_MAX ? -1 : c.bad_edge;
   if (c.bad_rows) return fail(WBPR_EINVAL, "row_offsets are not a valid CSR offset array");
   if (bad_edge >= 0)
-    return fail(WBPR_EINVAL, "edge " + std::to_string(bad_edge) + " has an out-of-range column or a negative capacity");
+    return fail(WBPR_EINVAL, "edge " + std::to_string(bad_edge) +
+                                 " has a column outside its instance's range or a negative capacity");
   a.maxlen = c.maxlen;
   if (layout == WBPR_LAYOUT_BCSR) {
     a.H = 2 * L.m - c.selfloops;
     build_bcsr(a, st);
+    build_bcsr_mate(a, st);
     CK(cudaGetLastError());
-    s = read_ctrl(W.ctrl, c, st);
-    if (s) return s;
-    M = c.M; Mf = c.M;
-    if (c.overflow == 1) return fail(WBPR_EOVERFLOW, "merged capacity exceeds INT32_MAX");
-    build_bcsr_mate(a, M, st);
-    CK(cudaGetLastError());
-    s = read_ctrl(W.ctrl, c, st);
-    if (s) return s;
-    if (c.overflow == 2) return fail(WBPR_EINTERNAL, "reverse arc not found while building mate[]");
+    Mf = -1;   // on the device
   } else {
     a.H = L.m;
     build_rcsr_forward(a, st);
@@ -162,7 +150,6 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
     if (s) return s;
     build_rcsr_reverse(a, Mf, c.maxlen, st);
     CK(cudaGetLastError());
-    M = 2 * Mf;
   }
   return WBPR_OK;
 }
@@ -236,6 +223,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   if (s) return s;
   const Layout& L = W.L;
 
+  const long long launches0 = launch_count();
   Events E;
   CK(E.create());
   CK(cudaEventRecord(E.ev[0], st));
@@ -253,7 +241,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
     col = at<int32_t>(ws, L.in_col);
     cap = at<int32_t>(ws, L.in_cap);
   }
-  k_init_ctrl<<<1, 256, 0, st>>>(W.ctrl);
+  { k_init_ctrl<<<1, 256, 0, st>>>(W.ctrl); note_launch(); }
   long long* d_s = at<long long>(ws, L.inst_s);
   long long* d_t = at<long long>(ws, L.inst_t);
   int64_t* d_vb = at<int64_t>(ws, L.vbase);
@@ -262,29 +250,34 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   CK(cudaMemcpyAsync(d_vb, vbase_h, 8 * (k + 1), cudaMemcpyHostToDevice, st));
   uint8_t* term = at<uint8_t>(ws, L.term);
   CK(cudaMemsetAsync(term, 0, n, st));
-  k_terms<<<(k + 255) / 256, 256, 0, st>>>(term, d_s, d_t, k);
-  if (k > 1) k_check_ranges<<<std::min(k, di.num_sms * 8), 256, 0, st>>>(ro, col, n, d_vb, k, W.ctrl);
+  { k_terms<<<(k + 255) / 256, 256, 0, st>>>(term, d_s, d_t, k); note_launch(); }
   CK(cudaGetLastError());
 
-  int M = 0, Mf = 0;
+  int Mf = 0;
   int64_t selfloops = 0, bad_edge = -1;
-  s = build_residual(W, ro, col, cap, opt.layout, di.num_sms, M, Mf, selfloops, bad_edge, st);
+  s = build_residual(W, ro, col, cap, opt.layout, di.num_sms, d_vb, k, Mf, selfloops, bad_edge, st);
   if (stats) { memset(stats, 0, sizeof(*stats)); stats->bad_edge_index = bad_edge; stats->n = n; stats->m = m; }
   if (s) return s;
-  register_view(W, opt.layout, M, Mf);
   CK(cudaEventRecord(E.ev[1], st));
   if (build_only) {
-    CK(cudaStreamSynchronize(st));
+    Ctrl cb;
+    s = read_ctrl(W.ctrl, cb, st);
+    if (s) return s;
+    const int M = opt.layout == WBPR_LAYOUT_BCSR ? cb.M : 2 * Mf;
+    register_view(W, opt.layout, M, opt.layout == WBPR_LAYOUT_BCSR ? cb.M : Mf);
+    if (cb.overflow == 1) return fail(WBPR_EOVERFLOW, "merged capacity exceeds INT32_MAX");
+    if (cb.overflow == 2) return fail(WBPR_EINTERNAL, "reverse arc not found while building mate[]");
     if (stats) {
       stats->M = M; stats->self_loops_ignored = selfloops;
       float ms = 0; cudaEventElapsedTime(&ms, E.ev[0], E.ev[1]); stats->build_ms = ms; stats->total_ms = ms;
+      stats->kernel_launches = launch_count() - launches0;
     }
     return WBPR_OK;
   }
 
   SolveParams P{};
   P.ctrl = W.ctrl;
-  P.n = (int)n; P.k = k; P.layout = opt.layout; P.M = M; P.Mf = Mf;
+  P.n = (int)n; P.k = k; P.layout = opt.layout; P.M = 0; P.Mf = Mf;
   P.off = at<int>(ws, L.off);
   P.arc = at<int2>(ws, L.regC);
   P.mate = at<int>(ws, L.regB);
@@ -301,8 +294,10 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.hist = at<int>(ws, L.hist);
   P.src = d_s; P.snk = d_t;
   P.max_rounds = opt.max_rounds > 0 ? opt.max_rounds : 10 * n + 1000;
-  P.gr_threshold = (unsigned long long)((double)opt.gr_beta * (double)(n + M)) + 1;
+  P.gr_beta = opt.gr_beta;
   P.gap_mode = opt.gap_mode;
+  P.push_mode = opt.push_mode;
+  P.gr_gamma = opt.gr_gamma;
   P.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
   int occ = di.occ[opt.layout];
   if (occ < 1) return fail(WBPR_ECUDA, "solve kernel cannot be resident on this device");
@@ -327,6 +322,10 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   CK(cudaMemcpyAsync(&c, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
 
+  const int M = opt.layout == WBPR_LAYOUT_BCSR ? c.M : 2 * Mf;
+  register_view(W, opt.layout, M, opt.layout == WBPR_LAYOUT_BCSR ? c.M : Mf);
+  if (c.overflow == 1) return fail(WBPR_EOVERFLOW, "merged capacity exceeds INT32_MAX");
+  if (c.overflow == 2) return fail(WBPR_EINTERNAL, "reverse arc not found while building mate[]");
   long long F = 0, C = 0;
   bool cert = true;
   for (int i = 0; i < k; ++i) {
@@ -358,6 +357,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
     cudaEventElapsedTime(&ms, E.ev[0], E.ev[3]); stats->total_ms = ms;
     stats->grid_blocks = blocks;
     stats->block_threads = kSolveThreads;
+    stats->kernel_launches = launch_count() - launches0;
   }
   if (c.status == DS_NOTCONVERGED) return fail(WBPR_ENOTCONVERGED, "round cap exceeded");
   if (c.abort) return fail(WBPR_ENOTCONVERGED, "device watchdog timeout");
@@ -380,6 +380,8 @@ wbpr_status wbpr_default_options(wbpr_options* opt) {
   opt->max_rounds = 0;
   opt->grid_blocks = 0;
   opt->timeout_ms = 120000;
+  opt->push_mode = 1;
+  opt->gr_gamma = 1.0f;
   return WBPR_OK;
 }
 
@@ -446,7 +448,7 @@ wbpr_status wbpr_bipartite_match(int64_t nL, int64_t nR, int64_t E, const int32_
   int64_t* ro = at<int64_t>(workspace, L.in_row);
   int32_t* col = at<int32_t>(workspace, L.in_col);
   int32_t* cap = at<int32_t>(workspace, L.in_cap);
-  k_init_ctrl<<<1, 256, 0, st>>>(ctrl);
+  { k_init_ctrl<<<1, 256, 0, st>>>(ctrl); note_launch(); }
   bip_validate(nL, nR, E, l, r, deg, cursor, ctrl, di.num_sms, st);
   CK(cudaGetLastError());
   Ctrl c;

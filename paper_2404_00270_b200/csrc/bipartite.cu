@@ -89,8 +89,8 @@ void bip_extract(const SolveParams& p, int64_t nL, int64_t nR, int32_t* match_of
   cudaMemsetAsync(match_of_left, 0xff, sizeof(int32_t) * nL, st);
   unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nR + T - 1) / T, num_sms * 32));
   if (nR <= 0) return;
-  if (p.layout == 0) k_bip_extract_bcsr<<<g, T, 0, st>>>(p.off, p.arc, nL, nR, match_of_left);
-  else k_bip_extract_rcsr<<<g, T, 0, st>>>(p.off, p.arc, p.roff, p.rarc, p.bcf, nL, nR, match_of_left);
+  if (p.layout == 0) { k_bip_extract_bcsr<<<g, T, 0, st>>>(p.off, p.arc, nL, nR, match_of_left); note_launch(); }
+  else { k_bip_extract_rcsr<<<g, T, 0, st>>>(p.off, p.arc, p.roff, p.rarc, p.bcf, nL, nR, match_of_left); note_launch(); }
 }
 
 // Validation + left-degree histogram (first offending edge lands in ctrl->bad_edge).
@@ -100,7 +100,7 @@ void bip_validate(int64_t nL, int64_t nR, int64_t E, const int32_t* l, const int
   cudaMemsetAsync(deg, 0, sizeof(int) * (nL + 1), st);
   cudaMemsetAsync(cursor, 0, sizeof(int) * (nL + 1), st);
   unsigned gE = (unsigned)std::max<int64_t>(1, std::min<int64_t>((E + T - 1) / T, num_sms * 32));
-  if (E > 0) k_bip_hist<<<gE, T, 0, st>>>(l, r, E, nL, nR, deg, ctrl);
+  if (E > 0) { k_bip_hist<<<gE, T, 0, st>>>(l, r, E, nL, nR, deg, ctrl); note_launch(); }
 }
 
 // Network CSR (after a successful validation).
@@ -110,10 +110,10 @@ void bip_build(int64_t nL, int64_t nR, int64_t E, const int32_t* l, const int32_
   exclusive_scan(deg, nL, scan_part, st);   // deg[nL] = E
   int64_t n = nL + nR + 2;
   unsigned gN = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 1 + T - 1) / T, num_sms * 32));
-  k_bip_rows<<<gN, T, 0, st>>>(deg, nL, nR, E, ro);
+  { k_bip_rows<<<gN, T, 0, st>>>(deg, nL, nR, E, ro); note_launch(); }
   int64_t mx = std::max(std::max(nL, nR), E);
   unsigned gS = (unsigned)std::max<int64_t>(1, std::min<int64_t>((mx + T - 1) / T, num_sms * 32));
-  k_bip_scatter<<<gS, T, 0, st>>>(l, r, E, nL, nR, deg, cursor, col, cap);
+  { k_bip_scatter<<<gS, T, 0, st>>>(l, r, E, nL, nR, deg, cursor, col, cap); note_launch(); }
 }
 
 }  // namespace wbpr

@@ -48,17 +48,29 @@ constexpr int kEdgesPerThread = 8;
 // Validation + in-degree histogram of the non-self-loop half-arcs.
 __global__ void k_edges(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
                         const int32_t* __restrict__ cap, int64_t n, int64_t m, int* indeg, Ctrl* ctrl,
-                        int count_in) {
+                        int count_in, const int64_t* __restrict__ vbase, int k) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t i0 = t * kEdgesPerThread;
   int loops = 0;
   if (i0 < m) {
     int64_t u = row_of(ro, n, i0);
+    // batch (A10): the instance [lo, hi) owning row u; edges must stay inside it
+    int64_t lo = 0, hi = n;
+    if (k > 1) {
+      int a = 0, b = k;
+      while (b - a > 1) { int mid = (a + b) >> 1; if (__ldg(vbase + mid) <= u) a = mid; else b = mid; }
+      lo = __ldg(vbase + a); hi = __ldg(vbase + a + 1);
+    }
     int64_t i1 = i0 + kEdgesPerThread < m ? i0 + kEdgesPerThread : m;
     for (int64_t i = i0; i < i1; ++i) {
       while (__ldg(ro + u + 1) <= i) ++u;
+      while (u >= hi) {
+        int a = 0, b = k;
+        while (b - a > 1) { int mid = (a + b) >> 1; if (__ldg(vbase + mid) <= u) a = mid; else b = mid; }
+        lo = __ldg(vbase + a); hi = __ldg(vbase + a + 1);
+      }
       int v = col[i], c = cap[i];
-      if (v < 0 || v >= n || c < 0) {
+      if (v < lo || v >= hi || c < 0) {
         atomicMin((unsigned long long*)&ctrl->bad_edge, (unsigned long long)i);
         continue;
       }
@@ -172,11 +184,19 @@ __global__ void k_merge_write(const uint64_t* __restrict__ keys, int64_t H, cons
   }
 }
 
+// Dense copy of the merged columns (region A, free after the merge) for the searches.
+__global__ void k_colcopy(const int2* __restrict__ arc, const Ctrl* ctrl, int* colv) {
+  const int M = ctrl->M;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < M; p += gridDim.x * blockDim.x) colv[p] = arc[p].x;
+}
+
 // mate[p] = position of the owner u inside seg(col[p]) — binary search on the
-// sorted segment, once per slot.  8 consecutive slots per thread
+// sorted segment, done once per arc PAIR: the slot with the smaller
+// endpoint searches and writes both directions.  8 consecutive slots per thread
 // share one owner search.
-__global__ void k_mate(const int* __restrict__ off, const int2* __restrict__ arc, int n, int M, int* mate,
-                       Ctrl* ctrl) {
+__global__ void k_mate(const int* __restrict__ off, const int* __restrict__ colv, int n, const Ctrl* ctrl_c,
+                       int* mate, Ctrl* ctrl) {
+  const int M = ctrl_c->M;
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t p0 = t * kEdgesPerThread;
   if (p0 >= M) return;
@@ -184,14 +204,16 @@ __global__ void k_mate(const int* __restrict__ off, const int2* __restrict__ arc
   int p1 = (int)(p0 + kEdgesPerThread < (int64_t)M ? p0 + kEdgesPerThread : (int64_t)M);
   for (int p = (int)p0; p < p1; ++p) {
     while (__ldg(off + u + 1) <= p) ++u;
-    int v = arc[p].x;
-    int lo = __ldg(off + v), hi = __ldg(off + v + 1);
+    int v = __ldg(colv + p);
+    if (v < u) continue;          // the pair is handled from its smaller endpoint
+    int lo = __ldg(off + v), end = __ldg(off + v + 1), hi = end;
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
-      if (arc[mid].x < u) lo = mid + 1; else hi = mid;
+      if (__ldg(colv + mid) < u) lo = mid + 1; else hi = mid;
     }
-    if (lo >= __ldg(off + v + 1) || arc[lo].x != u) { atomicExch(&ctrl->overflow, 2); lo = p; }
+    if (lo >= end || __ldg(colv + lo) != u) { atomicExch(&ctrl->overflow, 2); continue; }
     mate[p] = lo;
+    mate[lo] = p;
   }
 }
 
@@ -243,12 +265,12 @@ static unsigned grid_exact(int64_t items, int threads) {
 // deg[] and fills ctrl->{bad_edge, bad_rows, selfloops, maxlen}.
 void build_validate(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
-  k_rows<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.ro, a.n, a.m, a.deg, a.ctrl);
+  { k_rows<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.ro, a.n, a.m, a.deg, a.ctrl); note_launch(); }
   int64_t threads = (a.m + kEdgesPerThread - 1) / kEdgesPerThread;
   if (a.m > 0)
-    k_edges<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, a.n, a.m, a.deg, a.ctrl,
-                                                   a.layout == 0 ? 1 : 0);
-  k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl);
+    { k_edges<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, a.n, a.m, a.deg, a.ctrl,
+                                                   a.layout == 0 ? 1 : 0, a.vbase, a.k); note_launch(); }
+  { k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl); note_launch(); }
 }
 
 // Phase 2 (after the host checked the validation record): sort, merge, mate.
@@ -262,38 +284,40 @@ void build_bcsr(const BuildArgs& a, cudaStream_t st) {
   cudaMemsetAsync(a.cursor, 0, sizeof(int) * n, st);
   int64_t threads = (m + kEdgesPerThread - 1) / kEdgesPerThread;
   if (m > 0)
-    k_scatter_bcsr<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, a.soff, a.cursor, a.keys);
-  segmented_sort(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.ctrl, (int2*)a.arc, a.q0, a.num_sms, st);
+    { k_scatter_bcsr<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, a.soff, a.cursor, a.keys); note_launch(); }
+  segmented_sort(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.ctrl, a.arc, a.arc + a.H / 2, a.q0, a.num_sms, st);
   int* flags = (int*)a.tmp;
   cudaMemsetAsync(flags, 0, sizeof(int) * (H + 1), st);
-  k_rowstarts<<<grid_for(n, T, a.num_sms), T, 0, st>>>(a.soff, n, flags);
-  if (H > 0) k_heads<<<grid_for(H, T, a.num_sms, 32), T, 0, st>>>(a.keys, H, flags);
+  { k_rowstarts<<<grid_for(n, T, a.num_sms), T, 0, st>>>(a.soff, n, flags); note_launch(); }
+  if (H > 0) { k_heads<<<grid_for(H, T, a.num_sms, 32), T, 0, st>>>(a.keys, H, flags); note_launch(); }
   exclusive_scan(flags, H, a.scan_part, st);
-  k_newoff<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.soff, flags, n, a.off);
-  if (H > 0) k_merge_write<<<grid_for(H, T, a.num_sms, 32), T, 0, st>>>(a.keys, H, flags, a.arc, a.cap0, a.ctrl);
+  { k_newoff<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.soff, flags, n, a.off); note_launch(); }
+  if (H > 0) { k_merge_write<<<grid_for(H, T, a.num_sms, 32), T, 0, st>>>(a.keys, H, flags, a.arc, a.cap0, a.ctrl); note_launch(); }
   cudaMemcpyAsync(&a.ctrl->M, flags + H, sizeof(int), cudaMemcpyDeviceToDevice, st);
 }
 
-void build_bcsr_mate(const BuildArgs& a, int M, cudaStream_t st) {
+void build_bcsr_mate(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
-  int64_t threads = ((int64_t)M + kEdgesPerThread - 1) / kEdgesPerThread;
-  if (M > 0) k_mate<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.arc, (int)a.n, M, a.mate, a.ctrl);
+  // M is on the device (ctrl->M); H bounds it
+  { k_colcopy<<<grid_for(a.H, T, a.num_sms, 32), T, 0, st>>>(a.arc, a.ctrl, a.colv); note_launch(); }
+  int64_t threads = (a.H + kEdgesPerThread - 1) / kEdgesPerThread;
+  if (a.H > 0) { k_mate<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.colv, (int)a.n, a.ctrl, a.mate, a.ctrl); note_launch(); }
 }
 
 void build_rcsr_forward(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
   const int64_t n = a.n, m = a.m;
-  k_ro_to_i32<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.ro, n, a.soff);
+  { k_ro_to_i32<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.ro, n, a.soff); note_launch(); }
   int64_t threads = (m + kEdgesPerThread - 1) / kEdgesPerThread;
-  if (m > 0) k_keys_fwd<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, a.keys);
-  segmented_sort(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.ctrl, (int2*)a.arc, a.q0, a.num_sms, st);
+  if (m > 0) { k_keys_fwd<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, a.keys); note_launch(); }
+  segmented_sort(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.ctrl, a.arc, a.arc + a.H / 2, a.q0, a.num_sms, st);
   int* flags = (int*)a.tmp;
   cudaMemsetAsync(flags, 0, sizeof(int) * (m + 1), st);
-  k_rowstarts<<<grid_for(n, T, a.num_sms), T, 0, st>>>(a.soff, n, flags);
-  if (m > 0) k_heads<<<grid_for(m, T, a.num_sms, 32), T, 0, st>>>(a.keys, m, flags);
+  { k_rowstarts<<<grid_for(n, T, a.num_sms), T, 0, st>>>(a.soff, n, flags); note_launch(); }
+  if (m > 0) { k_heads<<<grid_for(m, T, a.num_sms, 32), T, 0, st>>>(a.keys, m, flags); note_launch(); }
   exclusive_scan(flags, m, a.scan_part, st);
-  k_newoff<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.soff, flags, n, a.off);
-  if (m > 0) k_merge_write<<<grid_for(m, T, a.num_sms, 32), T, 0, st>>>(a.keys, m, flags, a.arc, a.cap0, a.ctrl);
+  { k_newoff<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.soff, flags, n, a.off); note_launch(); }
+  if (m > 0) { k_merge_write<<<grid_for(m, T, a.num_sms, 32), T, 0, st>>>(a.keys, m, flags, a.arc, a.cap0, a.ctrl); note_launch(); }
   cudaMemcpyAsync(&a.ctrl->M, flags + m, sizeof(int), cudaMemcpyDeviceToDevice, st);
 }
 
@@ -302,9 +326,9 @@ void build_rcsr_forward(const BuildArgs& a, cudaStream_t st) {
 void build_rcsr_reverse_counts(const BuildArgs& a, int Mf, cudaStream_t st) {
   const int T = 256;
   cudaMemsetAsync(a.deg, 0, sizeof(int) * a.n, st);
-  if (Mf > 0) k_rdeg<<<grid_for(Mf, T, a.num_sms, 32), T, 0, st>>>(a.arc, Mf, a.deg);
+  if (Mf > 0) { k_rdeg<<<grid_for(Mf, T, a.num_sms, 32), T, 0, st>>>(a.arc, Mf, a.deg); note_launch(); }
   cudaMemsetAsync(&a.ctrl->maxlen, 0, sizeof(int), st);
-  k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl);
+  { k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl); note_launch(); }
   cudaMemcpyAsync(a.roff, a.deg, sizeof(int) * a.n, cudaMemcpyDeviceToDevice, st);
   exclusive_scan(a.roff, a.n, a.scan_part, st);
 }
@@ -314,9 +338,9 @@ void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st)
   cudaMemsetAsync(a.cursor, 0, sizeof(int) * a.n, st);
   int64_t threads = ((int64_t)Mf + kEdgesPerThread - 1) / kEdgesPerThread;
   if (Mf > 0)
-    k_scatter_rev<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.arc, (int)a.n, Mf, a.roff, a.cursor, a.keys);
-  segmented_sort(a.keys, a.tmp, a.roff, (int)a.n, maxlen, a.ctrl, a.rarc, a.q0, a.num_sms, st);
-  if (Mf > 0) k_write_rarc<<<grid_for(Mf, T, a.num_sms, 32), T, 0, st>>>(a.keys, Mf, a.rarc, a.bcf);
+    { k_scatter_rev<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.arc, (int)a.n, Mf, a.roff, a.cursor, a.keys); note_launch(); }
+  segmented_sort(a.keys, a.tmp, a.roff, (int)a.n, maxlen, a.ctrl, a.rarc, a.rarc + a.m / 2, a.q0, a.num_sms, st);
+  if (Mf > 0) { k_write_rarc<<<grid_for(Mf, T, a.num_sms, 32), T, 0, st>>>(a.keys, Mf, a.rarc, a.bcf); note_launch(); }
 }
 
 }  // namespace wbpr

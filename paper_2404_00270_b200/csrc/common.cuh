@@ -35,6 +35,28 @@ WBPR_DEV int ld_volatile(const int* p) { int v; asm volatile("ld.volatile.global
 
 template <typename T> WBPR_DEV T ld_nc(const T* p) { return __ldg(p); }
 
+// L2 eviction-priority hints (createpolicy + .L2::cache_hint): streamed arrays (arcs,
+// mate, queues) are loaded evict_first so they do not push the label array h[] (the
+// random-gather target, a few MB to ~70 MB) out of the 126 MB L2.
+WBPR_DEV unsigned long long policy_evict_first() {
+  unsigned long long p; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p;
+}
+WBPR_DEV unsigned long long policy_evict_last() {
+  unsigned long long p; asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p)); return p;
+}
+WBPR_DEV int2 ld_cg_hint(const int2* p, unsigned long long pol) {
+  int2 v; asm volatile("ld.global.cg.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol)); return v;
+}
+WBPR_DEV int ld_cg_hint(const int* p, unsigned long long pol) {
+  int v; asm volatile("ld.global.cg.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
+}
+WBPR_DEV int ld_nc_hint(const int* p, unsigned long long pol) {
+  int v; asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
+}
+WBPR_DEV int2 ld_nc_hint(const int2* p, unsigned long long pol) {
+  int2 v; asm volatile("ld.global.nc.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol)); return v;
+}
+
 WBPR_DEV unsigned long long globaltimer() {
   unsigned long long t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t;
 }
@@ -64,42 +86,11 @@ template <typename T> __device__ T block_sum(T v, T* smem /* >= 32 */) {
 }
 
 // ----------------------------------------------------------------- grid barrier
-// Software barrier for a cooperative (co-resident) grid.  The last arriving CTA
-// resets the count and bumps the generation.  Waiters back off with nanosleep and
-// give up after the watchdog deadline, setting *abort (never hangs the device).
+// Arrival counter of the software grid barrier of the persistent solve kernel
+// (protocol in solve.cu).
 struct GridBarrier {
   unsigned count;
   unsigned gen;
 };
-
-WBPR_DEV bool grid_sync(GridBarrier* b, unsigned nblocks, unsigned& gen, int* abort,
-                        unsigned long long deadline) {
-  __syncthreads();
-  __shared__ int s_abort;
-  if (threadIdx.x == 0) {
-    int ab = 0;
-    __threadfence();
-    unsigned arrived = atomicAdd(&b->count, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(&b->count, 0u);
-      __threadfence();
-      atomicAdd(&b->gen, 1u);
-    } else {
-      unsigned ns = 8;
-      while (ld_acquire(&b->gen) == gen) {
-        if (ld_volatile(abort)) { ab = 1; break; }
-        if (globaltimer() > deadline) { atomicExch(abort, 1); ab = 1; break; }
-        __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
-      }
-    }
-    __threadfence();
-    if (!ab) ab = ld_volatile(abort);
-    s_abort = ab;
-  }
-  gen++;
-  __syncthreads();
-  return s_abort == 0;
-}
 
 }  // namespace wbpr

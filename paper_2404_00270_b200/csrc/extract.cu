@@ -66,14 +66,14 @@ void extract_results(const SolveParams& p, const int64_t* ro, const int32_t* col
     int64_t words = (p.n + 31) / 32;
     int64_t blocks = (words * 32 + T - 1) / T;
     if (blocks > num_sms * 16) blocks = num_sms * 16;
-    k_bitmap<<<(unsigned)blocks, T, 0, st>>>(p.h, p.n, p.n, bitmap);
+    { k_bitmap<<<(unsigned)blocks, T, 0, st>>>(p.h, p.n, p.n, bitmap); note_launch(); }
   }
   cudaMemsetAsync(inst_cut, 0, sizeof(long long) * k, st);
   if (m > 0) {
     int64_t threads = (m + kCutEdges - 1) / kCutEdges;
-    k_cutcap<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(ro, col, cap, p.n, m, p.h, p.n, vbase, k, inst_cut);
+    { k_cutcap<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(ro, col, cap, p.n, m, p.h, p.n, vbase, k, inst_cut); note_launch(); }
   }
-  k_flows<<<(k + T - 1) / T, T, 0, st>>>(p.e, p.snk, k, inst_flow);
+  { k_flows<<<(k + T - 1) / T, T, 0, st>>>(p.e, p.snk, k, inst_flow); note_launch(); }
 }
 
 }  // namespace wbpr

@@ -20,17 +20,39 @@ constexpr uint8_t kSink = 2;
 
 // Per-phase counters, triple-buffered by phase parity (see solve.cu).
 struct Ring {
-  unsigned long long work;  // relabel work (slots scanned by relabels)
   int qn;                   // appended normal queue entries
   int hn;                   // appended huge vertices
   int hc;                   // appended huge chunk tasks
+  unsigned work;            // relabel work (slots scanned by relabels), saturating
+  int kind;                 // 1 = push/relabel round
   int pad[3];
+};
+
+// What the last CTA to arrive at a grid barrier publishes for everyone (one 16-B
+// release store; waiters poll it with 16-B acquire loads).
+struct __align__(16) Bcast {
+  unsigned gen;
+  int qn;
+  int hc;
+  unsigned flags;   // bit 0: a global relabel is due (decided by the last arriver)
+};
+
+enum PhaseKind { PK_NONE = 0, PK_ROUND = 1, PK_GR_RESET = 2, PK_BFS = 3, PK_COMPACT = 4, PK_PREFLOW = 5 };
+
+// Global-relabel policy state, written only by the last CTA to arrive at a barrier.
+struct GrPolicy {
+  unsigned long long work_since_gr;
+  unsigned long long t_gr_start;
+  unsigned long long t_after_gr;
+  unsigned long long gr_time;
 };
 
 // Huge-vertex record for one round: chunk tasks fold their partial minima into
 // `best` and the last chunk (done == nchunks) performs the push or relabel.
 struct HugeRec {
   unsigned long long best;  // (h << 32) | slot
+  long long spent;          // discharge: excess reserved by the chunks
+  long long pushed;         // discharge: excess actually pushed by the chunks
   int u;
   int nchunks;
   int done;
@@ -47,9 +69,12 @@ enum DevStatus { DS_OK = 0, DS_NOTCONVERGED = 1, DS_TIMEOUT = 2, DS_INTERNAL = 3
 // Device control block at the start of the workspace.
 struct Ctrl {
   GridBarrier bar;
+  int pad_bar[2];
+  Bcast bc;
   int abort;
   int status;
   Ring ring[3];
+  GrPolicy pol;
   long long excess_total;
   long long stats[ST_COUNT];
   // build info
@@ -62,7 +87,8 @@ struct Ctrl {
   int selfloops;
   int hub_chunks;         // build scratch counter
   int sort_items;         // build scratch counter
-  int pad0[6];
+  int sort_items_med;     // build scratch counter
+  int pad0[5];
   long long gap_level;    // online gap: lowest empty level seen this round (A6)
 };
 
@@ -134,8 +160,10 @@ struct SolveParams {
   const long long* src; // sources [k]
   const long long* snk; // sinks [k]
   long long max_rounds;
-  unsigned long long gr_threshold;
+  float gr_beta;         // GR when relabel work since the last GR >= gr_beta * (n + M)
+  float gr_gamma;        // GR when round time since the last GR >= gr_gamma * (last GR time)
   int gap_mode;
+  int push_mode;         // 0: one push to the lowest neighbour (Alg. 2); 1: warp-parallel discharge
   unsigned long long deadline_ns_rel;
 };
 

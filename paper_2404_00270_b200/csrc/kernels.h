@@ -7,10 +7,14 @@
 
 namespace wbpr {
 
+// number of kernels this library launched (process-wide; bench's gpu_launches)
+void note_launch();
+long long launch_count();
+
 void exclusive_scan(int* a, int64_t N, int* part, cudaStream_t st);
 
 void segmented_sort(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl,
-                    int2* items, int* big, int num_sms, cudaStream_t st);
+                    int2* items, int2* items_med, int* big, int num_sms, cudaStream_t st);
 
 struct BuildArgs {
   int64_t n, m, H;
@@ -35,11 +39,14 @@ struct BuildArgs {
   int2* rarc;      // region C + 8m (RCSR)
   int* bcf;        // region B (RCSR)
   int maxlen;
+  const int64_t* vbase;  // batch instance ranges (device), k entries + 1
+  int k;
+  int* colv;             // dense copy of the merged columns (region A after the merge)
 };
 
 void build_validate(const BuildArgs& a, cudaStream_t st);
 void build_bcsr(const BuildArgs& a, cudaStream_t st);
-void build_bcsr_mate(const BuildArgs& a, int M, cudaStream_t st);
+void build_bcsr_mate(const BuildArgs& a, cudaStream_t st);
 void build_rcsr_forward(const BuildArgs& a, cudaStream_t st);
 void build_rcsr_reverse_counts(const BuildArgs& a, int Mf, cudaStream_t st);
 void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st);

@@ -4,7 +4,13 @@
 #include "internal.h"
 #include "kernels.h"
 
+#include <atomic>
+
 namespace wbpr {
+
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = kScanTile / kScanThreads;  // 16
@@ -93,9 +99,9 @@ void exclusive_scan(int* a, int64_t N, int* part, cudaStream_t st) {
     return;
   }
   int64_t ntiles = (N + kScanTile - 1) / kScanTile;
-  k_scan_reduce<<<(unsigned)ntiles, kScanThreads, 0, st>>>(a, N, part);
-  k_scan_partials<<<1, 1024, 0, st>>>(part, ntiles);
-  k_scan_down<<<(unsigned)ntiles, kScanThreads, 0, st>>>(a, N, part, ntiles);
+  { k_scan_reduce<<<(unsigned)ntiles, kScanThreads, 0, st>>>(a, N, part); note_launch(); }
+  { k_scan_partials<<<1, 1024, 0, st>>>(part, ntiles); note_launch(); }
+  { k_scan_down<<<(unsigned)ntiles, kScanThreads, 0, st>>>(a, N, part, ntiles); note_launch(); }
 }
 
 }  // namespace wbpr

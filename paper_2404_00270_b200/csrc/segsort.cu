@@ -6,7 +6,9 @@
 //
 // Segment classes (lengths from 1 to ~1.6e5 at R-MAT scale 22):
 //   len <= 32        one warp per segment, rank sort in registers (32 shuffles)
-//   32 < len <= 4096 one CTA per segment, bitonic sort in shared memory
+//   32 < len <= 256  one warp per segment, register bitonic sort (8 keys per lane,
+//                    shuffles for the cross-lane stages, no shared memory / barriers)
+//   256 < len <= 4096 one CTA per segment, bitonic sort in shared memory
 //   len > 4096       4096-key chunks sorted as above, then log2(len/4096)
 //                    merge passes (merge-path co-rank, 8 outputs per thread),
 //                    ping-ponging between keys and tmp.
@@ -36,12 +38,71 @@ __global__ void __launch_bounds__(256) k_sort_warp(uint64_t* keys, const int* __
   }
 }
 
-// Enumerate CTA sort items: segments with 32 < len <= tile as one item, longer
-// segments as ceil(len/tile) chunk items; longer segments also go to `big`.
-__global__ void k_sort_items(const int* __restrict__ off, int nseg, int2* items, int* big, Ctrl* ctrl) {
+constexpr int kMedLen = 256;   // warp register sort up to this length
+
+// 32 < len <= 256: bitonic network over 256 keys held as r[j] = element j*32 + lane.
+__global__ void __launch_bounds__(256) k_sort_med(uint64_t* keys, const int2* __restrict__ items,
+                                                  const Ctrl* ctrl) {
+  const int nitems = ctrl->sort_items_med;
+  int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  int lane = lane_id();
+  for (int it = wg; it < nitems; it += nw) {
+    int2 item = items[it];
+    int beg = item.x, len = item.y;
+    uint64_t r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int e = j * 32 + lane;
+      r[j] = e < len ? keys[beg + e] : ~0ull;
+    }
+#pragma unroll
+    for (int k = 2; k <= kMedLen; k <<= 1) {
+#pragma unroll
+      for (int jj = k >> 1; jj > 0; jj >>= 1) {
+        if (jj >= 32) {
+          const int dj = jj >> 5;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if ((j & dj) == 0) {
+              int e = j * 32 + lane;
+              bool up = (e & k) == 0;
+              uint64_t a = r[j], b = r[j | dj];
+              if ((a > b) == up) { r[j] = b; r[j | dj] = a; }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            int e = j * 32 + lane;
+            uint64_t o = __shfl_xor_sync(FULL, r[j], jj);
+            bool up = (e & k) == 0;
+            bool lower = (lane & jj) == 0;
+            uint64_t mn = r[j] < o ? r[j] : o, mx = r[j] < o ? o : r[j];
+            r[j] = (lower == up) ? mn : mx;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int e = j * 32 + lane;
+      if (e < len) keys[beg + e] = r[j];
+    }
+  }
+}
+
+// Enumerate sort items: 32 < len <= 256 -> warp items; 256 < len <= tile -> CTA item;
+// longer segments -> ceil(len/tile) CTA chunk items and the `big` list.
+__global__ void k_sort_items(const int* __restrict__ off, int nseg, int2* items, int2* items_med, int* big,
+                             Ctrl* ctrl) {
   for (int sgi = blockIdx.x * blockDim.x + threadIdx.x; sgi < nseg; sgi += gridDim.x * blockDim.x) {
     int beg = off[sgi], len = off[sgi + 1] - beg;
     if (len <= 32) continue;
+    if (len <= kMedLen) {
+      items_med[atomicAdd(&ctrl->sort_items_med, 1)] = make_int2(beg, len);
+      continue;
+    }
     int nit = (len + kSortTile - 1) / kSortTile;
     int idx = atomicAdd(&ctrl->sort_items, nit);
     for (int c = 0; c < nit; ++c) {
@@ -60,7 +121,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tile(uint64_t* keys, cons
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     int2 item = items[it];
     int beg = item.x, len = item.y;
-    int P = 64;
+    int P = 512;
     while (P < len) P <<= 1;
     for (int i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < len ? keys[beg + i] : ~0ull;
     __syncthreads();
@@ -136,33 +197,36 @@ __global__ void __launch_bounds__(256) k_copy_big(const uint64_t* __restrict__ s
 }
 
 void segmented_sort(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl,
-                    int2* items, int* big, int num_sms, cudaStream_t st) {
+                    int2* items, int2* items_med, int* big, int num_sms, cudaStream_t st) {
   if (nseg <= 0 || maxlen < 2) return;
   cudaMemsetAsync(&ctrl->sort_items, 0, sizeof(int), st);
+  cudaMemsetAsync(&ctrl->sort_items_med, 0, sizeof(int), st);
   cudaMemsetAsync(&ctrl->hub_chunks, 0, sizeof(int), st);
   {
     int64_t warps = nseg;
     int64_t blocks = (warps * 32 + 255) / 256;
     if (blocks > (int64_t)num_sms * 64) blocks = (int64_t)num_sms * 64;
-    k_sort_warp<<<(unsigned)blocks, 256, 0, st>>>(keys, off, nseg);
+    { k_sort_warp<<<(unsigned)blocks, 256, 0, st>>>(keys, off, nseg); note_launch(); }
   }
   if (maxlen <= 32) return;
   {
     int64_t blocks = (nseg + 255) / 256;
     if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
-    k_sort_items<<<(unsigned)blocks, 256, 0, st>>>(off, nseg, items, big, ctrl);
+    { k_sort_items<<<(unsigned)blocks, 256, 0, st>>>(off, nseg, items, items_med, big, ctrl); note_launch(); }
   }
-  k_sort_tile<<<num_sms * 4, kTileThreads, 0, st>>>(keys, items, ctrl);
+  { k_sort_med<<<num_sms * 16, 256, 0, st>>>(keys, items_med, ctrl); note_launch(); }
+  if (maxlen <= kMedLen) return;
+  { k_sort_tile<<<num_sms * 4, kTileThreads, 0, st>>>(keys, items, ctrl); note_launch(); }
   if (maxlen <= kSortTile) return;
   const uint64_t* src = keys;
   uint64_t* dst = tmp;
   int passes = 0;
   for (int w = kSortTile; w < maxlen; w <<= 1) {
-    k_merge_pass<<<num_sms * 8, 256, 0, st>>>(src, dst, off, big, ctrl, w);
+    { k_merge_pass<<<num_sms * 8, 256, 0, st>>>(src, dst, off, big, ctrl, w); note_launch(); }
     const uint64_t* t = src; src = dst; dst = const_cast<uint64_t*>(t);
     ++passes;
   }
-  if (passes & 1) k_copy_big<<<num_sms * 8, 256, 0, st>>>(tmp, keys, off, big, ctrl);
+  if (passes & 1) { k_copy_big<<<num_sms * 8, 256, 0, st>>>(tmp, keys, off, big, ctrl); note_launch(); }
 }
 
 }  // namespace wbpr

@@ -45,19 +45,21 @@ struct Seg {
 
 struct BcsrOps {
   const int* off; int2* arc; const int* mate;
+  unsigned long long pf = 0;   // L2 evict_first policy for streamed arrays
+  __device__ void init() { pf = policy_evict_first(); }
   __device__ Seg seg(int u) const { Seg s; s.fb = __ldg(off + u); s.fe = __ldg(off + u + 1); s.rb = s.re = 0; return s; }
   __device__ int degree(int u) const { return __ldg(off + u + 1) - __ldg(off + u); }
   // residual out-arc #i of u: u -> col with residual capacity cf, identified by slot
   __device__ void out_arc(const Seg& s, int i, int& col, int& cf, int& slot) const {
     slot = s.fb + i;
-    int2 a = ld_cg(arc + slot);
+    int2 a = ld_cg_hint(arc + slot, pf);
     col = a.x; cf = a.y;
   }
   // residual in-arc #i of w: col -> w with capacity cf(col -> w)
   __device__ void in_arc(const Seg& s, int i, int& col, int& cf) const {
     int p = s.fb + i;
-    col = __ldg(&arc[p].x);
-    cf = ld_cg(&arc[__ldg(mate + p)].y);
+    col = ld_nc_hint(&arc[p].x, pf);
+    cf = ld_cg(&arc[ld_nc_hint(mate + p, pf)].y);
   }
   __device__ void col_cf_of_slot(int slot, int& col, int& cf) const {
     int2 a = ld_cg(arc + slot); col = a.x; cf = a.y;
@@ -71,6 +73,8 @@ struct BcsrOps {
 
 struct RcsrOps {
   const int* foff; int2* farc; const int* roff; const int2* rarc; int* bcf; int Mf;
+  unsigned long long pf = 0;
+  __device__ void init() { pf = policy_evict_first(); }
   __device__ Seg seg(int u) const {
     Seg s; s.fb = __ldg(foff + u); s.fe = __ldg(foff + u + 1); s.rb = __ldg(roff + u); s.re = __ldg(roff + u + 1);
     return s;
@@ -82,11 +86,11 @@ struct RcsrOps {
     int df = s.fe - s.fb;
     if (i < df) {
       slot = s.fb + i;
-      int2 a = ld_cg(farc + slot);
+      int2 a = ld_cg_hint(farc + slot, pf);
       col = a.x; cf = a.y;
     } else {
       int q = s.rb + (i - df);
-      int2 r = __ldg(rarc + q);            // {col, flow_idx}
+      int2 r = ld_nc_hint(rarc + q, pf);   // {col, flow_idx}
       col = r.x;
       cf = ld_cg(bcf + r.y);               // backward cf: flow on col -> u that can return
       slot = Mf + q;
@@ -96,10 +100,10 @@ struct RcsrOps {
     int df = s.fe - s.fb;
     if (i < df) {                          // w -> col forward: col -> w is its backward arc
       int p = s.fb + i;
-      col = __ldg(&farc[p].x);
+      col = ld_nc_hint(&farc[p].x, pf);
       cf = ld_cg(bcf + p);
     } else {                               // col -> w forward arc f
-      int2 r = __ldg(rarc + s.rb + (i - df));
+      int2 r = ld_nc_hint(rarc + s.rb + (i - df), pf);
       col = r.x;
       cf = ld_cg(&farc[r.y].y);
     }
@@ -114,16 +118,39 @@ struct RcsrOps {
   }
 };
 
-// ------------------------------------------------------------------ warp append buffers
+// ------------------------------------------------------------------ grid barrier
+// Arrival: one acq_rel atomic per CTA.  The last CTA to arrive reads the counters
+// the finished phase accumulated, zeroes the ring slot the phase after next will
+// use, and publishes {generation, counts} with ONE 16-B release store; waiters poll
+// that word with 16-B acquire loads, so the counts arrive together with the
+// release (no extra round trip after the barrier).  Waiters give up at the
+// watchdog deadline or when another CTA aborted (never hangs the device).
+WBPR_DEV unsigned atom_add_acqrel(unsigned* p, unsigned v) {
+  unsigned o;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory");
+  return o;
+}
+WBPR_DEV uint4 ld_acquire_v4(const Bcast* p) {
+  uint4 r;
+  asm volatile("ld.acquire.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
+WBPR_DEV void st_release_v4(Bcast* p, uint4 v) {
+  asm volatile("st.release.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+
 struct SharedState {
   int buf[kWarps][kBufCap];
-  int cnt[kWarps];
   int wsum[kWarps];
   unsigned long long wsum64[kWarps];
   int base;
-  Ring ring;          // post-barrier broadcast of the finalized ring slot
+  int abort;
+  Bcast bc;           // counts of the phase that just finished
 };
 
+// ------------------------------------------------------------------ warp append buffers
 struct QueueOut {   // next-queue destination
   int* q; int* qn;
   HugeRec* hq; int2* hc; int* hn; int* hc_cnt;
@@ -157,20 +184,12 @@ __device__ __forceinline__ void huge_append(int u, int deg, const QueueOut& out)
   int nch = (deg + kChunk - 1) / kChunk;
   int hi = atomicAdd(out.hn, 1);
   int c0 = atomicAdd(out.hc_cnt, nch);
-  HugeRec r; r.best = ~0ull; r.u = u; r.nchunks = nch; r.done = 0; r.pad = 0;
+  HugeRec r; r.best = ~0ull; r.spent = 0; r.pushed = 0; r.u = u; r.nchunks = nch; r.done = 0; r.pad = 0;
   out.hq[hi] = r;
   for (int j = 0; j < nch; ++j) out.hc[c0 + j] = make_int2(hi, j);
 }
 
 // ------------------------------------------------------------------ the kernel
-template <class Ops>
-struct Solver {
-  const SolveParams& P;
-  Ops ops;
-  __device__ Solver(const SolveParams& p, const Ops& o) : P(p), ops(o) {}
-};
-
-template <class Ops>
 __device__ __forceinline__ void block_flush_all(SharedState& S, int& cnt, const QueueOut& out) {
   // block-aggregated final flush: one global atomic per CTA
   int lane = lane_id(), w = warp_id();
@@ -185,7 +204,6 @@ __device__ __forceinline__ void block_flush_all(SharedState& S, int& cnt, const 
   int base = S.base + S.wsum[w];
   for (int i = lane; i < cnt; i += 32) st_cg(out.q + base + i, S.buf[w][i]);
   cnt = 0;
-  __syncthreads();
 }
 
 __device__ __forceinline__ unsigned long long block_sum_u64(SharedState& S, unsigned long long v) {
@@ -200,10 +218,15 @@ __device__ __forceinline__ unsigned long long block_sum_u64(SharedState& S, unsi
 }
 
 template <class Ops>
-__global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, const Ops ops) {
+__global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, const Ops ops_in) {
   __shared__ SharedState S;
+  Ops ops = ops_in;
+  ops.init();
+  const unsigned long long pl = policy_evict_last();   // keep h[] in L2
   Ctrl* C = P.ctrl;
   const int N = P.n;
+  const unsigned long long gr_threshold =
+      (unsigned long long)((double)P.gr_beta * (double)((long long)N + (long long)ld_cg((const int*)&C->M))) + 1;
   const unsigned nb = gridDim.x;
   const int lane = lane_id(), w = warp_id();
   const int gwarp = blockIdx.x * kWarps + w;
@@ -211,34 +234,73 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
   unsigned gen = 0;
   int ph = 0;
   const unsigned long long deadline = globaltimer() + P.deadline_ns_rel;
-  // per-warp statistics (registers)
+  // per-warp statistics (registers; lane 0 holds the counts)
   long long st_push = 0, st_relabel = 0, st_arcs = 0, st_bfs_arcs = 0, st_cand = 0;
   int cnt = 0;  // this warp's staged appends (lane-uniform)
 
-  auto ring = [&](int p) -> Ring* { return &C->ring[((p % 3) + 3) % 3]; };
+  auto ring = [&](int p) -> Ring* { return &C->ring[p % 3]; };
   auto out_for = [&](int buf) {
     QueueOut o;
-    o.q = P.q[buf]; o.qn = &ring(ph)->qn;
-    o.hq = P.hq[buf]; o.hc = P.hc[buf]; o.hn = &ring(ph)->hn; o.hc_cnt = &ring(ph)->hc;
+    Ring* r = ring(ph);
+    o.q = P.q[buf]; o.qn = &r->qn;
+    o.hq = P.hq[buf]; o.hc = P.hc[buf]; o.hn = &r->hn; o.hc_cnt = &r->hc;
     return o;
   };
-  // barrier + ring rotation + broadcast of the finalized counters
   auto gsync = [&]() -> bool {
-    bool ok = grid_sync(&C->bar, nb, gen, &C->abort, deadline);
-    ++ph;
-    if (threadIdx.x == 0) {
-      Ring* r = ring(ph - 1);
-      S.ring.work = ld_cg(&r->work);
-      S.ring.qn = ld_cg(&r->qn);
-      S.ring.hn = ld_cg(&r->hn);
-      S.ring.hc = ld_cg(&r->hc);
-      if (blockIdx.x == 0) {
-        Ring* z = ring(ph + 1);
-        z->work = 0; z->qn = 0; z->hn = 0; z->hc = 0;
-      }
-    }
     __syncthreads();
-    return ok;
+    if (threadIdx.x == 0) {
+      const unsigned target = gen + 1;
+      int ab = 0;
+      uint4 b;
+      unsigned old = atom_add_acqrel(&C->bar.count, 1u);
+      if (old == nb - 1) {
+        C->bar.count = 0;
+        Ring* r = ring(ph);
+        const int qn = ld_cg(&r->qn), hc = ld_cg(&r->hc), kind = ld_cg(&r->kind);
+        const unsigned long long now = globaltimer();
+        GrPolicy& G = C->pol;
+        unsigned flags = 0;
+        if (kind == PK_ROUND) {
+          atomicAdd((unsigned long long*)&C->stats[ST_AVQ], (unsigned long long)(qn + ld_cg(&r->hn)));
+          G.work_since_gr += ld_cg(&r->work);
+          // GR policy (reading §8(c) #8): queue empty, relabel work above
+          // beta (n + M), or time spent in rounds since the last GR above gamma x its cost
+          bool due = qn + hc == 0 || G.work_since_gr >= gr_threshold ||
+                     (P.gr_gamma > 0.f && (double)(now - G.t_after_gr) >= (double)P.gr_gamma * (double)G.gr_time);
+          if (due) { flags = 1; G.t_gr_start = now; }
+        } else if (kind == PK_PREFLOW) {
+          G.t_gr_start = now;
+        } else if (kind == PK_COMPACT) {
+          G.gr_time = now - G.t_gr_start;
+          G.t_after_gr = now;
+          G.work_since_gr = 0;
+        }
+        b.x = target;
+        b.y = (unsigned)qn;
+        b.z = (unsigned)hc;
+        b.w = flags;
+        Ring* z = ring(ph + 1);
+        z->qn = 0; z->hn = 0; z->hc = 0; z->work = 0; z->kind = 0;
+        st_release_v4(&C->bc, b);
+      } else {
+        unsigned ns = 0;
+        while (true) {
+          b = ld_acquire_v4(&C->bc);
+          if (b.x == target) break;
+          if (ld_volatile(&C->abort)) { ab = 1; break; }
+          if (globaltimer() > deadline) { atomicExch(&C->abort, 1); ab = 1; break; }
+          if (ns) __nanosleep(ns);
+          ns = ns ? (ns < 128 ? ns * 2 : 128) : 16;
+        }
+      }
+      if (!ab) ab = ld_volatile(&C->abort);
+      S.abort = ab;
+      S.bc.qn = (int)b.y; S.bc.hc = (int)b.z; S.bc.flags = b.w;
+    }
+    ++gen;
+    ++ph;
+    __syncthreads();
+    return S.abort == 0;
   };
 
   // ---------------------------------------------------------------- init
@@ -267,21 +329,20 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
     }
     unsigned long long t = block_sum_u64(S, exc);
     if (threadIdx.x == 0 && t) atomicAdd((unsigned long long*)&C->excess_total, t);
+    if (blockIdx.x == 0 && threadIdx.x == 0) ring(ph)->kind = PK_PREFLOW;
   }
   if (!gsync()) return;
 
   long long rounds = 0;
-  unsigned long long work_since_gr = 0;
   int cur = 0;          // queue buffer holding the current AVQ
   bool need_gr = true;
-  bool done = false;
 
-  while (!done) {
+  while (true) {
     if (need_gr) {
       // ------------------------------------------------------------ global relabel
       // reset labels: sinks 0, everything else |V| (= unreached); frontier <- sinks
       for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x)
-        st_cg(P.h + v, (__ldg(P.term + v) & kSink) ? 0 : N);
+        st_cg(P.h + v, (__ldg(P.term + v) & kSink) ? 0 : ((__ldg(P.term + v) & kSource) ? N + 1 : N));
       if (blockIdx.x == 0) {
         QueueOut o = out_for(0);
         for (int base = w * 32; base < P.k; base += kWarps * 32) {
@@ -292,13 +353,13 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
           if (huge) huge_append(t, dg, o);
           warp_append(S, cnt, i < P.k && !huge, t, o);
         }
-        block_flush_all<Ops>(S, cnt, o);
+        block_flush_all(S, cnt, o);
+        if (threadIdx.x == 0) { C->stats[ST_GRS]++; ring(ph)->kind = PK_GR_RESET; }
       }
-      if (blockIdx.x == 0 && threadIdx.x == 0) C->stats[ST_GRS]++;
       if (!gsync()) return;
       int fb = 0, level = 0;
       while (true) {
-        int qn = S.ring.qn, hc = S.ring.hc;
+        int qn = S.bc.qn, hc = S.bc.hc;
         if (qn + hc == 0) break;
         QueueOut o = out_for(fb ^ 1);
         const int* qf = P.q[fb];
@@ -317,7 +378,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
             sg = ops.seg(wv);
             lo = c.y * kChunk; hi = min(sg.deg(), lo + kChunk);
           }
-          st_bfs_arcs += hi - lo;
+          if (lane == 0) st_bfs_arcs += hi - lo;
           for (int b = lo; b < hi; b += 32) {
             int i = b + lane;
             bool found = false;
@@ -325,7 +386,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
             if (i < hi) {
               int cf;
               ops.in_arc(sg, i, u, cf);
-              if (cf > 0 && __ldg(P.term + u) == 0 && ld_cg(P.h + u) == N) {
+              if (cf > 0 && ld_cg_hint(P.h + u, pl) == N) {   // sinks 0, sources N+1: never N
                 if (atomicCAS(P.h + u, N, level + 1) == N) {   // level(u) = level(w) + 1
                   found = true;
                   dg = ops.degree(u);
@@ -337,8 +398,8 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
             warp_append(S, cnt, found && !huge, u, o);
           }
         }
-        block_flush_all<Ops>(S, cnt, o);
-        if (blockIdx.x == 0 && threadIdx.x == 0) C->stats[ST_BFS_LEVELS]++;
+        block_flush_all(S, cnt, o);
+        if (blockIdx.x == 0 && threadIdx.x == 0) { C->stats[ST_BFS_LEVELS]++; ring(ph)->kind = PK_BFS; }
         if (!gsync()) return;
         fb ^= 1;
         ++level;
@@ -366,62 +427,125 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
               }
             }
           }
-          st_cand += min(32, N - base);
+          if (lane == 0) st_cand += min(32, N - base);
           if (huge) huge_append(v, dg, o);
           warp_append(S, cnt, act && !huge, v, o);
         }
-        block_flush_all<Ops>(S, cnt, o);
+        block_flush_all(S, cnt, o);
         unsigned long long t = block_sum_u64(S, dropped);
         if (threadIdx.x == 0 && t) atomicAdd((unsigned long long*)&C->excess_total, (unsigned long long)(-(long long)t));
+        if (blockIdx.x == 0 && threadIdx.x == 0) ring(ph)->kind = PK_COMPACT;
       }
       if (!gsync()) return;
       cur = 0;
-      work_since_gr = 0;
       need_gr = false;
       // termination: right after an exact GR, no active vertex <=> e(s)+e(t) >= Excess_total
-      if (S.ring.qn + S.ring.hn == 0) { done = true; break; }
+      if (S.bc.qn + S.bc.hc == 0) break;
     }
 
     // -------------------------------------------------------------- one push/relabel round
     {
-      int qn = S.ring.qn, hc = S.ring.hc;
+      const int qn = S.bc.qn, hc = S.bc.hc;
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         C->stats[ST_ROUNDS]++;
-        C->stats[ST_AVQ] += qn + S.ring.hn;
+        ring(ph)->kind = PK_ROUND;
       }
       QueueOut o = out_for(cur ^ 1);
       const int* qc = P.q[cur];
       HugeRec* hqc = P.hq[cur];
       const int2* hcc = P.hc[cur];
       unsigned long long work = 0;
-      int total = qn + hc;
+      const int total = qn + hc;
       for (int tk = gwarp; tk < total; tk += nwarps) {
         int u, lo, hi, hidx = -1;
-        Seg sg;
         if (tk < qn) {
           u = ld_cg(qc + tk);
-          sg = ops.seg(u); lo = 0; hi = sg.deg();
         } else {
           int2 c = ld_cg(hcc + (tk - qn));
           hidx = c.x;
+          lo = c.y * kChunk;
           u = ld_cg(&hqc[hidx].u);
-          sg = ops.seg(u);
-          lo = c.y * kChunk; hi = min(sg.deg(), lo + kChunk);
         }
-        st_arcs += hi - lo;
-        // second-level parallelism: lanes scan the residual arcs, keep (h, slot) minimum
-        unsigned long long best = ~0ull;
+        // independent loads issued together: segment bounds, h(u), e(u)
+        Seg sg = ops.seg(u);
+        const int hu = ld_cg(P.h + u);
+        const long long eu = ld_cg(P.e + u);
+        if (hidx < 0) { lo = 0; hi = sg.deg(); } else { hi = min(sg.deg(), lo + kChunk); }
+        if (lane == 0) st_arcs += hi - lo;
+
+        unsigned long long best = ~0ull;   // (h, slot) minimum over residual arcs (Alg. 1 l.10-13)
         int bcf = 0, bcol = 0;
+        long long pushed = 0;              // discharge: excess moved by this warp
+        if (P.push_mode == 0) {
+          // ---- second-level parallelism: lanes scan the residual arcs
 #pragma unroll 2
-        for (int i = lo + lane; i < hi; i += 32) {
-          int col, cf, slot;
-          ops.out_arc(sg, i, col, cf, slot);
-          if (cf > 0) {
-            unsigned hv = (unsigned)ld_cg(P.h + col);
-            unsigned long long cand = ((unsigned long long)hv << 32) | (unsigned)slot;
-            if (cand < best) { best = cand; bcf = cf; bcol = col; }
+          for (int i = lo + lane; i < hi; i += 32) {
+            int col, cf, slot;
+            ops.out_arc(sg, i, col, cf, slot);
+            if (cf > 0) {
+              unsigned hv = (unsigned)ld_cg_hint(P.h + col, pl);
+              unsigned long long cand = ((unsigned long long)hv << 32) | (unsigned)slot;
+              if (cand < best) { best = cand; bcf = cf; bcol = col; }
+            }
+          }
+        } else {
+          // ---- warp-parallel discharge: every admissible arc (h(v) < h(u), relaxed rule
+          // P:187-189) of this 32-slot group receives part of the remaining budget, split
+          // by an exclusive prefix sum of the residual capacities in slot order.
+          long long snap = eu;             // lower bound of e(u) (only u's warps decrease it)
+          long long budget = eu;           // normal task: local budget
+          for (int b0 = lo; b0 < hi; b0 += 32) {
+            int i = b0 + lane;
+            int col = 0, cf = 0, slot = 0, hv = INT_MAX;
+            if (i < hi) {
+              ops.out_arc(sg, i, col, cf, slot);
+              if (cf > 0) {
+                hv = ld_cg_hint(P.h + col, pl);
+                unsigned long long cand = ((unsigned long long)(unsigned)hv << 32) | (unsigned)slot;
+                if (cand < best) { best = cand; bcf = cf; bcol = col; }
+              }
+            }
+            bool adm = cf > 0 && hv < hu;
+            unsigned am = __ballot_sync(FULL, adm);
+            if (!am) continue;
+            long long c = adm ? cf : 0;
+            long long incl = c;
+#pragma unroll
+            for (int o2 = 1; o2 < 32; o2 <<= 1) {
+              long long y = __shfl_up_sync(FULL, incl, o2);
+              if (lane >= o2) incl += y;
+            }
+            long long want = __shfl_sync(FULL, incl, 31);
+            long long avail;
+            if (hidx < 0) {
+              avail = budget;
+            } else {
+              long long got = 0;
+              if (lane == 0) got = (long long)atomicAdd((unsigned long long*)&hqc[hidx].spent, (unsigned long long)want);
+              got = __shfl_sync(FULL, got, 0);
+              avail = snap - got;
+              if (avail < 0) avail = 0;
+            }
+            long long excl = incl - c;
+            long long d = adm ? (avail - excl < c ? avail - excl : c) : 0;
+            bool app = false;
+            if (d > 0) {
+              ops.push(slot, (int)d);
+              long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col), (unsigned long long)d);
+              app = old_v == 0 && __ldg(P.term + col) == 0;
+              ++st_push;
+            }
+            long long used = want < avail ? want : avail;
+            pushed += used;
+            budget -= used;
+            int dgv = app ? ops.degree(col) : 0;
+            bool hugev = app && dgv > kChunk;
+            if (hugev) huge_append(col, dgv, o);
+            warp_append(S, cnt, app && !hugev, col, o);
+            if (hidx < 0 && budget <= 0) break;
           }
         }
+        // warp minimum (redux.sync) of the (h, slot) candidates
         unsigned hmin = __reduce_min_sync(FULL, (unsigned)(best >> 32));
         unsigned smin = __reduce_min_sync(FULL, (unsigned)(best >> 32) == hmin ? (unsigned)best : kInf);
         unsigned long long wbest = ((unsigned long long)hmin << 32) | smin;
@@ -429,43 +553,46 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
         int src_lane = owner ? __ffs(owner) - 1 : 0;
         int cfv = __shfl_sync(FULL, bcf, src_lane);
         int colv = __shfl_sync(FULL, bcol, src_lane);
-        bool finalize = true;
         if (hidx >= 0) {
-          // fold this chunk's minimum into the vertex record; the last chunk finalizes
+          // fold this chunk into the vertex record; the last chunk finalizes
           int last = 0;
           if (lane == 0) {
             if (wbest != ~0ull) atomicMin(&hqc[hidx].best, wbest);
+            if (pushed) atomicAdd((unsigned long long*)&hqc[hidx].pushed, (unsigned long long)pushed);
             __threadfence();
             int nch = ld_cg(&hqc[hidx].nchunks);
             last = (atomicAdd(&hqc[hidx].done, 1) == nch - 1);
             if (last) {
               __threadfence();
               wbest = ld_cg(&hqc[hidx].best);
+              pushed = ld_cg(&hqc[hidx].pushed);
               if (wbest != ~0ull) ops.col_cf_of_slot((int)(wbest & 0xffffffffu), colv, cfv);
             }
           }
-          finalize = __shfl_sync(FULL, last, 0);
+          if (!__shfl_sync(FULL, last, 0)) continue;
           wbest = __shfl_sync(FULL, wbest, 0);
           colv = __shfl_sync(FULL, colv, 0);
           cfv = __shfl_sync(FULL, cfv, 0);
+          pushed = __shfl_sync(FULL, pushed, 0);
           hmin = (unsigned)(wbest >> 32);
         }
-        if (!finalize) continue;
         // delegated lane 0: push or relabel
         int app_u = -1, app_v = -1, dgu = 0, dgv = 0;
         if (lane == 0) {
-          int hu = ld_cg(P.h + u);
-          long long eu = ld_cg(P.e + u);
-          if (hmin != kInf && (int)hmin < hu && cfv > 0) {
+          if (P.push_mode == 0 && hmin != kInf && (int)hmin < hu && cfv > 0) {
             // push: d = min(e(u), c_f(u,v')) (Alg. 1 line 15), four atomics (lines 16-19)
+            const int dv = ops.degree(colv);
             int d = (int)(eu < (long long)cfv ? eu : (long long)cfv);
             int slot = (int)(wbest & 0xffffffffu);
             ops.push(slot, d);
             long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-(long long)d));
             long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + colv), (unsigned long long)d);
             if (old_u - d > 0) { app_u = u; dgu = sg.deg(); }
-            if (old_v == 0 && __ldg(P.term + colv) == 0) { app_v = colv; dgv = ops.degree(colv); }
+            if (old_v == 0 && __ldg(P.term + colv) == 0) { app_v = colv; dgv = dv; }
             ++st_push;
+          } else if (P.push_mode != 0 && pushed > 0) {
+            long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-pushed));
+            if (old_u - pushed > 0) { app_u = u; dgu = sg.deg(); }
           } else {
             // relabel: h(u) <- h' + 1 (Alg. 1 line 21); >= |V| deactivates
             int nh = (hmin == kInf || (int)hmin >= N - 1) ? N : (int)hmin + 1;
@@ -480,19 +607,18 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
         warp_append(S, cnt, lane == 0 && app_u >= 0, app_u, o);
         warp_append(S, cnt, lane == 0 && app_v >= 0, app_v, o);
       }
-      block_flush_all<Ops>(S, cnt, o);
+      block_flush_all(S, cnt, o);
       unsigned long long t = block_sum_u64(S, work);
-      if (threadIdx.x == 0 && t) atomicAdd(&ring(ph)->work, t);
+      if (threadIdx.x == 0 && t) atomicAdd(&ring(ph)->work, (unsigned)(t < 0x7fffffffull ? t : 0x7fffffffull));
       if (!gsync()) return;
       cur ^= 1;
       ++rounds;
-      work_since_gr += S.ring.work;
       if (rounds >= P.max_rounds) {
         if (blockIdx.x == 0 && threadIdx.x == 0) { C->status = DS_NOTCONVERGED; }
         break;
       }
-      // early break / periodic GR (reading §8(c) #8)
-      if (S.ring.qn + S.ring.hn == 0 || work_since_gr >= P.gr_threshold) need_gr = true;
+      // early break / periodic GR, decided by the barrier's last arriver
+      if (S.bc.flags & 1) need_gr = true;
     }
   }
 
@@ -518,6 +644,7 @@ int solve_max_blocks_per_sm(int layout, int threads) {
 }
 
 cudaError_t launch_solve(const SolveParams& p, int blocks, int threads, cudaStream_t st) {
+  note_launch();
   if (p.layout == 0) {
     BcsrOps o{p.off, p.arc, p.mate};
     void* args[] = {(void*)&p, (void*)&o};

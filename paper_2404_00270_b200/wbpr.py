@@ -43,7 +43,7 @@ class Csr(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int32), ("gr_beta", ctypes.c_float), ("gap_mode", ctypes.c_int32),
                 ("max_rounds", ctypes.c_int64), ("grid_blocks", ctypes.c_int32), ("timeout_ms", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("push_mode", ctypes.c_int32), ("gr_gamma", ctypes.c_float), ("reserved", ctypes.c_int32 * 4)]
 
 
 class Stats(ctypes.Structure):
@@ -52,7 +52,8 @@ class Stats(ctypes.Structure):
         "relabels", "arcs_scanned", "bfs_arcs_scanned", "compaction_candidates", "avq_total", "gap_lifts",
         "self_loops_ignored", "bad_edge_index", "excess_total")] + [
         ("build_ms", ctypes.c_float), ("solve_ms", ctypes.c_float), ("extract_ms", ctypes.c_float),
-        ("total_ms", ctypes.c_float), ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32)]
+        ("total_ms", ctypes.c_float), ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int64)]
 
     def as_dict(self):
         return {f[0]: getattr(self, f[0]) for f in self._fields_}
@@ -107,7 +108,7 @@ def _check(st: int):
 
 
 def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: int = 0, grid_blocks: int = 0,
-            timeout_ms: int = 0) -> Options:
+            timeout_ms: int = 0, push_mode: Optional[int] = None, gr_gamma: Optional[float] = None) -> Options:
     o = Options()
     _check(load().wbpr_default_options(ctypes.byref(o)))
     o.layout = _LAYOUTS[layout]
@@ -118,6 +119,10 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
     o.grid_blocks = grid_blocks
     if timeout_ms > 0:
         o.timeout_ms = timeout_ms
+    if push_mode is not None:
+        o.push_mode = push_mode
+    if gr_gamma is not None:
+        o.gr_gamma = gr_gamma
     return o
 
 

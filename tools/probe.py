@@ -17,6 +17,10 @@ def graph(name):
     if name == "c3h": return synth.rmat(22, 16, 1, "hub20")
     if name == "r18p": return synth.rmat(18, 16, 1000, "paper")
     if name == "r18h": return synth.rmat(18, 16, 1000, "hub20")
+    if name.startswith("path"):
+        k = int(name[4:])
+        src = np.arange(k - 1); dst = src + 1
+        return synth.from_edges(k, src, dst, np.ones(k - 1, np.int32), 0, k - 1, name=name)
     raise ValueError(name)
 
 
@@ -25,6 +29,9 @@ ap.add_argument("cfgs", nargs="+")
 ap.add_argument("--layout", default="bcsr")
 ap.add_argument("--beta", type=float, default=0.0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--blocks", type=int, default=0)
+ap.add_argument("--mode", type=int, default=1)
+ap.add_argument("--gamma", type=float, default=-1.0)
 ap.add_argument("--oracle", action="store_true")
 a = ap.parse_args()
 for name in a.cfgs:
@@ -35,7 +42,7 @@ for name in a.cfgs:
         gen = time.time() - t0
         for rep in range(a.reps):
             size, match, st = W.bipartite_match(1 << 20, 1 << 20, lt, rt, layout=a.layout, gr_beta=a.beta,
-                                                timeout_ms=100000)
+                                                timeout_ms=100000, grid_blocks=a.blocks, push_mode=a.mode, gr_gamma=a.gamma)
             print(json.dumps(dict(cfg=name, rep=rep, gen_s=round(gen, 2), size=size, **st)), flush=True)
         continue
     g = graph(name)
@@ -44,8 +51,8 @@ for name in a.cfgs:
     ws = W.Workspace(W.workspace_size(g.n, g.m, 1, W.options(a.layout)))
     for rep in range(a.reps):
         F, bm, st = W.maxflow(ro, col, cap, g.s, g.t, layout=a.layout, workspace=ws, gr_beta=a.beta,
-                              timeout_ms=100000)
-        print(json.dumps(dict(cfg=name, rep=rep, gen_s=round(gen, 2), n=g.n, m=g.m, **st)), flush=True)
+                              timeout_ms=100000, grid_blocks=a.blocks, push_mode=a.mode, gr_gamma=a.gamma)
+        print(json.dumps(dict(cfg=name, rep=rep, gen_s=round(gen, 2), **st)), flush=True)
     if a.oracle:
         import oracle
         r = oracle.maxflow_graph(g, phase2=False)
