@@ -179,6 +179,9 @@ def run_wbpr(args, rank, world, local_rank):
     col_h = torch.from_numpy(G.col).pin_memory()
     cap_h = torch.from_numpy(G.cap).pin_memory()
     opt = dict(layout=args.layout)
+    for kv in args.opt:
+        k_, v_ = kv.split("=")
+        opt[k_] = float(v_) if "." in v_ else int(v_)
     ws = W.Workspace(W.workspace_size(G.n, G.m, k, W.options(args.layout)), dev)
     bitmap_d = torch.empty((G.n + 31) // 32, dtype=torch.int32, device=dev)
     bitmap_h = torch.empty((G.n + 31) // 32, dtype=torch.int32).pin_memory()
@@ -290,7 +293,7 @@ def run_wbpr(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "int64",
         "data": "synthetic",
-        "config": {"workload": args.workload, "desc": wl["desc"], "layout": args.layout,
+        "config": {"workload": args.workload, "desc": wl["desc"], "layout": args.layout, "options": args.opt,
                    "instances_per_rank": k, "n_per_rank": int(G.n), "m_per_rank": int(G.m),
                    "parallelism": f"instances sharded over {world} rank(s); NCCL all_gather of 64-B records",
                    "l2": "inputs and workspace larger than L2 (126 MB)"},
@@ -388,6 +391,7 @@ def main():
     ap.add_argument("--impl", default="wbpr", choices=["wbpr", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--opt", action="append", default=[], help="solver option key=value (wbpr_options field)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -89,7 +89,13 @@ typedef struct wbpr_options {
   float gr_gamma;        /* also GR when the time spent in rounds since the last GR reaches
                             gr_gamma x the duration of that GR (balances the two; 0 = off);
                             < 0 -> default 1.0                                               */
-  int32_t reserved[4];
+  int32_t l2_persist;    /* 1: persisting L2 access-policy window over the label
+                            array h[] for the solve launch (sets the context's persisting-L2
+                            limit); 0 (default): off                                                */
+  int32_t bfs_mode;      /* global-relabel BFS: 0 top-down only; 1 (default) direction-
+                            optimizing (bottom-up levels while the frontier is large);
+                            2 bottom-up from the first level (testing)                      */
+  int32_t reserved[2];
 } wbpr_options;
 
 typedef struct wbpr_stats {

@@ -2,6 +2,7 @@
 // validation, workspace carving, launch orchestration and error mapping.
 // Each solve: K-BUILD kernels (A1) -> one cooperative persistent kernel (A2-A7)
 // -> extraction kernels (A8) -> one stream synchronisation.
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstring>
@@ -297,13 +298,44 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.gr_beta = opt.gr_beta;
   P.gap_mode = opt.gap_mode;
   P.push_mode = opt.push_mode;
+  P.bfs_mode = opt.bfs_mode;
   P.gr_gamma = opt.gr_gamma;
   P.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
   int occ = di.occ[opt.layout];
   if (occ < 1) return fail(WBPR_ECUDA, "solve kernel cannot be resident on this device");
   int blocks = di.num_sms * occ;
   if (opt.grid_blocks > 0 && opt.grid_blocks < blocks) blocks = opt.grid_blocks;
+  // Keep the label array h[] (the random-gather target of every scan and BFS step)
+  // resident in L2: a persisting access-policy window over h for the solve launch.
+  bool window = false;
+  {
+    int dev = 0, maxp = 0, maxw = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    size_t hb = sizeof(int) * (size_t)n;
+    if (maxp > 0 && maxw > 0 && opt.l2_persist) {
+      size_t lim = std::min((size_t)maxp, hb);
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim);
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.base_ptr = P.h;
+      v.accessPolicyWindow.num_bytes = std::min((size_t)maxw, hb);
+      v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)lim / (float)v.accessPolicyWindow.num_bytes);
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      window = cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+      cudaGetLastError();
+    }
+  }
   CK(launch_solve(P, blocks, kSolveThreads, st));
+  if (window) {
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    cudaGetLastError();
+  }
   CK(cudaEventRecord(E.ev[2], st));
 
   uint32_t* dbm = bitmap;
@@ -382,6 +414,8 @@ wbpr_status wbpr_default_options(wbpr_options* opt) {
   opt->timeout_ms = 120000;
   opt->push_mode = 1;
   opt->gr_gamma = 1.0f;
+  opt->l2_persist = 0;
+  opt->bfs_mode = 1;
   return WBPR_OK;
 }
 

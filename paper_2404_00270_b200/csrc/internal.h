@@ -24,8 +24,9 @@ struct Ring {
   int hn;                   // appended huge vertices
   int hc;                   // appended huge chunk tasks
   unsigned work;            // relabel work (slots scanned by relabels), saturating
-  int kind;                 // 1 = push/relabel round
-  int pad[3];
+  int kind;                 // PhaseKind of the phase that used this slot
+  unsigned fedges;          // BFS: residual slots of the vertices appended to the next frontier
+  int pad[2];
 };
 
 // What the last CTA to arrive at a grid barrier publishes for everyone (one 16-B
@@ -34,7 +35,7 @@ struct __align__(16) Bcast {
   unsigned gen;
   int qn;
   int hc;
-  unsigned flags;   // bit 0: a global relabel is due (decided by the last arriver)
+  unsigned flags;   // bit 0: a global relabel is due; bit 1: next BFS level bottom-up
 };
 
 enum PhaseKind { PK_NONE = 0, PK_ROUND = 1, PK_GR_RESET = 2, PK_BFS = 3, PK_COMPACT = 4, PK_PREFLOW = 5 };
@@ -45,6 +46,9 @@ struct GrPolicy {
   unsigned long long t_gr_start;
   unsigned long long t_after_gr;
   unsigned long long gr_time;
+  unsigned long long bfs_seen_edges;   // slots of the vertices labelled so far in this GR
+  int bfs_bottom_up;                   // direction of the current BFS level
+  int pad;
 };
 
 // Huge-vertex record for one round: chunk tasks fold their partial minima into
@@ -164,6 +168,7 @@ struct SolveParams {
   float gr_gamma;        // GR when round time since the last GR >= gr_gamma * (last GR time)
   int gap_mode;
   int push_mode;         // 0: one push to the lowest neighbour (Alg. 2); 1: warp-parallel discharge
+  int bfs_mode;          // 0: top-down only; 1: direction-optimizing; 2: bottom-up after level 0
   unsigned long long deadline_ns_rel;
 };
 

@@ -40,7 +40,57 @@ __global__ void __launch_bounds__(256) k_sort_warp(uint64_t* keys, const int* __
 
 constexpr int kMedLen = 256;   // warp register sort up to this length
 
-// 32 < len <= 256: bitonic network over 256 keys held as r[j] = element j*32 + lane.
+// Bitonic network over P = 32*NR keys held by one warp as r[j] = element j*32 + lane:
+// stages with partner distance >= 32 swap registers inside a lane, shorter ones
+// exchange with __shfl_xor_sync.  No shared memory, no barriers.
+template <int NR>
+__device__ __forceinline__ void warp_bitonic(uint64_t (&r)[NR], int lane) {
+  constexpr int P = 32 * NR;
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj >= 32) {
+        const int dj = jj >> 5;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          if ((j & dj) == 0) {
+            const bool up = ((j * 32 + lane) & k) == 0;
+            uint64_t a = r[j], b = r[j | dj];
+            if ((a > b) == up) { r[j] = b; r[j | dj] = a; }
+          }
+        }
+      } else {
+        const bool lower = (lane & jj) == 0;
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          uint64_t o = __shfl_xor_sync(FULL, r[j], jj);
+          const bool up = ((j * 32 + lane) & k) == 0;
+          uint64_t mn = r[j] < o ? r[j] : o, mx = r[j] < o ? o : r[j];
+          r[j] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
+template <int NR>
+__device__ __forceinline__ void warp_sort_segment(uint64_t* keys, int beg, int len, int lane) {
+  uint64_t r[NR];
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    int e = j * 32 + lane;
+    r[j] = e < len ? keys[beg + e] : ~0ull;
+  }
+  warp_bitonic<NR>(r, lane);
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    int e = j * 32 + lane;
+    if (e < len) keys[beg + e] = r[j];
+  }
+}
+
+// 32 < len <= 256: one warp per segment; network size adapted to the length.
 __global__ void __launch_bounds__(256) k_sort_med(uint64_t* keys, const int2* __restrict__ items,
                                                   const Ctrl* ctrl) {
   const int nitems = ctrl->sort_items_med;
@@ -49,46 +99,9 @@ __global__ void __launch_bounds__(256) k_sort_med(uint64_t* keys, const int2* __
   int lane = lane_id();
   for (int it = wg; it < nitems; it += nw) {
     int2 item = items[it];
-    int beg = item.x, len = item.y;
-    uint64_t r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int e = j * 32 + lane;
-      r[j] = e < len ? keys[beg + e] : ~0ull;
-    }
-#pragma unroll
-    for (int k = 2; k <= kMedLen; k <<= 1) {
-#pragma unroll
-      for (int jj = k >> 1; jj > 0; jj >>= 1) {
-        if (jj >= 32) {
-          const int dj = jj >> 5;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if ((j & dj) == 0) {
-              int e = j * 32 + lane;
-              bool up = (e & k) == 0;
-              uint64_t a = r[j], b = r[j | dj];
-              if ((a > b) == up) { r[j] = b; r[j | dj] = a; }
-            }
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            int e = j * 32 + lane;
-            uint64_t o = __shfl_xor_sync(FULL, r[j], jj);
-            bool up = (e & k) == 0;
-            bool lower = (lane & jj) == 0;
-            uint64_t mn = r[j] < o ? r[j] : o, mx = r[j] < o ? o : r[j];
-            r[j] = (lower == up) ? mn : mx;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int e = j * 32 + lane;
-      if (e < len) keys[beg + e] = r[j];
-    }
+    if (item.y <= 64) warp_sort_segment<2>(keys, item.x, item.y, lane);
+    else if (item.y <= 128) warp_sort_segment<4>(keys, item.x, item.y, lane);
+    else warp_sort_segment<8>(keys, item.x, item.y, lane);
   }
 }
 
@@ -114,35 +127,6 @@ __global__ void k_sort_items(const int* __restrict__ off, int nseg, int2* items,
   }
 }
 
-__global__ void __launch_bounds__(kTileThreads) k_sort_tile(uint64_t* keys, const int2* __restrict__ items,
-                                                             const Ctrl* ctrl) {
-  __shared__ uint64_t s[kSortTile];
-  int nitems = ctrl->sort_items;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-    int2 item = items[it];
-    int beg = item.x, len = item.y;
-    int P = 512;
-    while (P < len) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < len ? keys[beg + i] : ~0ull;
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < P; i += blockDim.x) {
-          int ixj = i ^ j;
-          if (ixj > i) {
-            uint64_t a = s[i], b = s[ixj];
-            bool up = (i & k) == 0;
-            if ((a > b) == up) { s[i] = b; s[ixj] = a; }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    for (int i = threadIdx.x; i < len; i += blockDim.x) keys[beg + i] = s[i];
-    __syncthreads();
-  }
-}
-
 // Smallest i in [max(0,k-lb), min(k,la)] with A[i] > B[k-i-1] (A wins ties): the
 // number of outputs among the first k that come from A.
 __device__ __forceinline__ int co_rank(int k, const uint64_t* A, int la, const uint64_t* B, int lb) {
@@ -153,6 +137,61 @@ __device__ __forceinline__ int co_rank(int k, const uint64_t* A, int la, const u
     if (A[i] <= B[k - i - 1]) lo = i + 1; else hi = i;
   }
   return lo;
+}
+
+// 256 < len <= 4096 (and 4096-key chunks of longer segments): one 512-thread CTA.
+// Each warp sorts a 256-key chunk in registers (warp_bitonic), then log2(chunks)
+// merge-path passes in shared memory (8 outputs per thread, co-rank search).
+constexpr int kCtaSmemBytes = 2 * kSortTile * 8;   // ping-pong buffers (64 KB)
+__global__ void __launch_bounds__(kTileThreads) k_sort_tile(uint64_t* keys, const int2* __restrict__ items,
+                                                             const Ctrl* ctrl) {
+  extern __shared__ uint64_t sm[];
+  uint64_t* A = sm;
+  uint64_t* B = sm + kSortTile;
+  const int nitems = ctrl->sort_items;
+  const int lane = lane_id(), w = warp_id();
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    int2 item = items[it];
+    const int beg = item.x, len = item.y;
+    const int nc = (len + kMedLen - 1) / kMedLen;          // 256-key chunks
+    if (w < nc) {
+      uint64_t r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int e = w * kMedLen + j * 32 + lane;
+        r[j] = e < len ? keys[beg + e] : ~0ull;
+      }
+      warp_bitonic<8>(r, lane);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) A[w * kMedLen + j * 32 + lane] = r[j];
+    }
+    __syncthreads();
+    const int total = nc * kMedLen;
+    uint64_t* src = A;
+    uint64_t* dst = B;
+    for (int wd = kMedLen; wd < total; wd <<= 1) {
+      for (int kk = threadIdx.x * 8; kk < total; kk += blockDim.x * 8) {
+        int pair0 = kk / (2 * wd) * (2 * wd);
+        int la = min(wd, total - pair0);
+        int lb = min(wd, total - pair0 - la);
+        if (lb < 0) lb = 0;
+        const uint64_t* SA = src + pair0;
+        const uint64_t* SB = SA + la;
+        int k = kk - pair0;
+        int i = co_rank(k, SA, la, SB, lb);
+        int j = k - i;
+        int outn = min(8, la + lb - k);
+        for (int q = 0; q < outn; ++q) {
+          bool takeA = j >= lb || (i < la && SA[i] <= SB[j]);
+          dst[kk + q] = takeA ? SA[i++] : SB[j++];
+        }
+      }
+      __syncthreads();
+      uint64_t* t = src; src = dst; dst = t;
+    }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) keys[beg + i] = src[i];
+    __syncthreads();
+  }
 }
 
 // One merge pass of width w over every big segment (one CTA per segment).
@@ -216,7 +255,9 @@ void segmented_sort(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int
   }
   { k_sort_med<<<num_sms * 16, 256, 0, st>>>(keys, items_med, ctrl); note_launch(); }
   if (maxlen <= kMedLen) return;
-  { k_sort_tile<<<num_sms * 4, kTileThreads, 0, st>>>(keys, items, ctrl); note_launch(); }
+  {
+    cudaFuncSetAttribute(k_sort_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmemBytes);
+    k_sort_tile<<<num_sms * 3, kTileThreads, kCtaSmemBytes, st>>>(keys, items, ctrl); note_launch(); }
   if (maxlen <= kSortTile) return;
   const uint64_t* src = keys;
   uint64_t* dst = tmp;

@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
   const unsigned long long pl = policy_evict_last();   // keep h[] in L2
   Ctrl* C = P.ctrl;
   const int N = P.n;
+  const int Mslots = P.layout == 0 ? ld_cg((const int*)&C->M) : 2 * P.Mf;
   const unsigned long long gr_threshold =
       (unsigned long long)((double)P.gr_beta * (double)((long long)N + (long long)ld_cg((const int*)&C->M))) + 1;
   const unsigned nb = gridDim.x;
@@ -270,6 +271,19 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
           if (due) { flags = 1; G.t_gr_start = now; }
         } else if (kind == PK_PREFLOW) {
           G.t_gr_start = now;
+        } else if (kind == PK_GR_RESET || kind == PK_BFS) {
+          // direction-optimizing BFS (Beamer): bottom-up while the frontier's slots
+          // exceed 1/14 of the slots not yet labelled; back to top-down when the
+          // frontier holds fewer than n/24 vertices
+          const unsigned long long fe = ld_cg(&r->fedges);
+          if (kind == PK_GR_RESET) { G.bfs_seen_edges = 0; G.bfs_bottom_up = 0; }
+          G.bfs_seen_edges += fe;
+          const unsigned long long Mtot = (unsigned long long)Mslots;
+          const unsigned long long rest = Mtot > G.bfs_seen_edges ? Mtot - G.bfs_seen_edges : 0;
+          if (!G.bfs_bottom_up) G.bfs_bottom_up = P.bfs_mode != 0 && fe * 14ull > rest;
+          else G.bfs_bottom_up = (long long)qn * 24 >= (long long)N;
+          if (P.bfs_mode == 2) G.bfs_bottom_up = 1;
+          if (G.bfs_bottom_up) flags |= 2;
         } else if (kind == PK_COMPACT) {
           G.gr_time = now - G.t_gr_start;
           G.t_after_gr = now;
@@ -280,7 +294,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
         b.z = (unsigned)hc;
         b.w = flags;
         Ring* z = ring(ph + 1);
-        z->qn = 0; z->hn = 0; z->hc = 0; z->work = 0; z->kind = 0;
+        z->qn = 0; z->hn = 0; z->hc = 0; z->work = 0; z->kind = 0; z->fedges = 0;
         st_release_v4(&C->bc, b);
       } else {
         unsigned ns = 0;
@@ -352,6 +366,8 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
           bool huge = i < P.k && dg > kChunk;
           if (huge) huge_append(t, dg, o);
           warp_append(S, cnt, i < P.k && !huge, t, o);
+          unsigned fsum = warp_sum((unsigned)dg);
+          if (lane == 0 && fsum) atomicAdd(&ring(ph)->fedges, fsum);
         }
         block_flush_all(S, cnt, o);
         if (threadIdx.x == 0) { C->stats[ST_GRS]++; ring(ph)->kind = PK_GR_RESET; }
@@ -362,41 +378,92 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
         int qn = S.bc.qn, hc = S.bc.hc;
         if (qn + hc == 0) break;
         QueueOut o = out_for(fb ^ 1);
-        const int* qf = P.q[fb];
-        const HugeRec* hqf = P.hq[fb];
-        const int2* hcf = P.hc[fb];
-        int total = qn + hc;
-        for (int tk = gwarp; tk < total; tk += nwarps) {
-          int wv, lo, hi;
-          Seg sg;
-          if (tk < qn) {
-            wv = ld_cg(qf + tk);
-            sg = ops.seg(wv); lo = 0; hi = sg.deg();
-          } else {
-            int2 c = ld_cg(hcf + (tk - qn));
-            wv = ld_cg(&hqf[c.x].u);
-            sg = ops.seg(wv);
-            lo = c.y * kChunk; hi = min(sg.deg(), lo + kChunk);
-          }
-          if (lane == 0) st_bfs_arcs += hi - lo;
-          for (int b = lo; b < hi; b += 32) {
-            int i = b + lane;
-            bool found = false;
-            int u = 0, dg = 0;
-            if (i < hi) {
-              int cf;
-              ops.in_arc(sg, i, u, cf);
-              if (cf > 0 && ld_cg_hint(P.h + u, pl) == N) {   // sinks 0, sources N+1: never N
-                if (atomicCAS(P.h + u, N, level + 1) == N) {   // level(u) = level(w) + 1
-                  found = true;
-                  dg = ops.degree(u);
+        unsigned fedges = 0;   // lane 0: slots of the vertices this warp appended
+        if (!(S.bc.flags & 2)) {
+          // ---- top-down: frontier vertex w, in-arcs u -> w with c_f > 0
+          const int* qf = P.q[fb];
+          const HugeRec* hqf = P.hq[fb];
+          const int2* hcf = P.hc[fb];
+          int total = qn + hc;
+          for (int tk = gwarp; tk < total; tk += nwarps) {
+            int wv, lo, hi;
+            Seg sg;
+            if (tk < qn) {
+              wv = ld_cg(qf + tk);
+              sg = ops.seg(wv); lo = 0; hi = sg.deg();
+            } else {
+              int2 c = ld_cg(hcf + (tk - qn));
+              wv = ld_cg(&hqf[c.x].u);
+              sg = ops.seg(wv);
+              lo = c.y * kChunk; hi = min(sg.deg(), lo + kChunk);
+            }
+            if (lane == 0) st_bfs_arcs += hi - lo;
+            for (int b = lo; b < hi; b += 32) {
+              int i = b + lane;
+              bool found = false;
+              int u = 0, dg = 0;
+              if (i < hi) {
+                int cf;
+                ops.in_arc(sg, i, u, cf);
+                if (cf > 0 && ld_cg_hint(P.h + u, pl) == N) {   // sinks 0, sources N+1: never N
+                  if (atomicCAS(P.h + u, N, level + 1) == N) {   // level(u) = level(w) + 1
+                    found = true;
+                    dg = ops.degree(u);
+                  }
                 }
               }
+              unsigned fsum = warp_sum((unsigned)dg);
+              if (lane == 0) fedges += fsum;
+              bool huge = found && dg > kChunk;
+              if (huge) huge_append(u, dg, o);
+              warp_append(S, cnt, found && !huge, u, o);
             }
-            bool huge = found && dg > kChunk;
-            if (huge) huge_append(u, dg, o);
-            warp_append(S, cnt, found && !huge, u, o);
           }
+        } else {
+          // ---- bottom-up: every unlabelled vertex v looks for an out-arc v -> w with
+          // c_f > 0 and level(w) = level (early exit per 32-slot group)
+          for (int base = (blockIdx.x * kWarps + w) * 32; base < N; base += nwarps * 32) {
+            int v = base + lane;
+            int hv = v < N ? ld_cg_hint(P.h + v, pl) : -1;
+            unsigned todo = __ballot_sync(FULL, hv == N);
+            unsigned found_mask = 0;
+            while (todo) {
+              int j = __ffs(todo) - 1;
+              todo &= todo - 1;
+              int vv = base + j;
+              Seg sg = ops.seg(vv);
+              int d = sg.deg();
+              bool hit = false;
+              int scanned = 0;
+              for (int b = 0; b < d; b += 32) {
+                int i = b + lane;
+                bool ok = false;
+                if (i < d) {
+                  int col, cf, slot;
+                  ops.out_arc(sg, i, col, cf, slot);
+                  ok = cf > 0 && ld_cg_hint(P.h + col, pl) == level;
+                }
+                scanned += 32;
+                if (__ballot_sync(FULL, ok)) { hit = true; break; }
+              }
+              if (lane == 0) st_bfs_arcs += min(scanned, d);
+              if (hit) {
+                found_mask |= 1u << j;
+                if (lane == 0) st_cg(P.h + vv, level + 1);
+              }
+            }
+            bool found = (found_mask >> lane) & 1u;
+            int dg = found ? ops.degree(v) : 0;
+            unsigned fsum = warp_sum((unsigned)dg);
+            if (lane == 0) fedges += fsum;
+            bool huge = found && dg > kChunk;
+            if (huge) huge_append(v, dg, o);
+            warp_append(S, cnt, found && !huge, v, o);
+          }
+        }
+        {
+          unsigned long long t = block_sum_u64(S, (unsigned long long)fedges);
+          if (threadIdx.x == 0 && t) atomicAdd(&ring(ph)->fedges, (unsigned)t);
         }
         block_flush_all(S, cnt, o);
         if (blockIdx.x == 0 && threadIdx.x == 0) { C->stats[ST_BFS_LEVELS]++; ring(ph)->kind = PK_BFS; }

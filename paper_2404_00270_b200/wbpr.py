@@ -43,7 +43,8 @@ class Csr(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int32), ("gr_beta", ctypes.c_float), ("gap_mode", ctypes.c_int32),
                 ("max_rounds", ctypes.c_int64), ("grid_blocks", ctypes.c_int32), ("timeout_ms", ctypes.c_int32),
-                ("push_mode", ctypes.c_int32), ("gr_gamma", ctypes.c_float), ("reserved", ctypes.c_int32 * 4)]
+                ("push_mode", ctypes.c_int32), ("gr_gamma", ctypes.c_float), ("l2_persist", ctypes.c_int32),
+                ("bfs_mode", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 class Stats(ctypes.Structure):
@@ -108,7 +109,8 @@ def _check(st: int):
 
 
 def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: int = 0, grid_blocks: int = 0,
-            timeout_ms: int = 0, push_mode: Optional[int] = None, gr_gamma: Optional[float] = None) -> Options:
+            timeout_ms: int = 0, push_mode: Optional[int] = None, gr_gamma: Optional[float] = None,
+            l2_persist: Optional[int] = None, bfs_mode: Optional[int] = None) -> Options:
     o = Options()
     _check(load().wbpr_default_options(ctypes.byref(o)))
     o.layout = _LAYOUTS[layout]
@@ -123,6 +125,10 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
         o.push_mode = push_mode
     if gr_gamma is not None:
         o.gr_gamma = gr_gamma
+    if l2_persist is not None:
+        o.l2_persist = l2_persist
+    if bfs_mode is not None:
+        o.bfs_mode = bfs_mode
     return o
 
 

@@ -150,6 +150,17 @@ def test_gr_frequency_and_grid_size_invariance(layout):
         assert_parity(g, layout, ref=ref, validate=False, gr_beta=beta, grid_blocks=blocks)
 
 
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("push_mode", [0, 1])
+@pytest.mark.parametrize("bfs_mode", [0, 1, 2])
+def test_modes(layout, push_mode, bfs_mode):
+    # the paper's single push (Alg. 2) and the discharge deviation; top-down, direction-
+    # optimizing and bottom-up BFS: all must reach the same unique F / cut / S*
+    for g in (synth.rmat(12, 16, 7, "hub20"), synth.grid(40, 30, True, 2),
+              synth.tiny_random(9, 30, 5, 3), synth.random_graph(800, 6000, 5, 0, 799)):
+        assert_parity(g, layout, push_mode=push_mode, bfs_mode=bfs_mode)
+
+
 # ------------------------------------------------------------------ host-buffer path (e2e)
 def test_host_buffers():
     import torch
