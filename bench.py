@@ -54,9 +54,9 @@ def make_workload(name, rank, world):
     """Returns dict(kind, parts|graph, ids, desc) for this rank."""
     import synth
     if name == "c5":
+        from paper_2404_00270_b200.batch import partition
         total = 64
-        per = total // world
-        lo, hi = rank * per, (rank + 1) * per if rank < world - 1 else total
+        lo, hi = partition(total, world, rank)
         parts = [synth.rmat(18, 16, 1000 + i, "paper") for i in range(lo, hi)]
         return dict(kind="batch", parts=parts, ids=list(range(lo, hi)), total=total,
                     desc="C5: 64 x R-MAT scale 18 (edgefactor 16, U[1,100] caps, 20 paper-rule s/t pairs "
@@ -66,7 +66,7 @@ def make_workload(name, rank, world):
          "c2r": lambda: synth.grid(1024, 1024, True, 1),
          "c3": lambda: synth.rmat(22, 16, 1, "paper"),
          "c3h": lambda: synth.rmat(22, 16, 1, "hub20")}[name]()
-    return dict(kind="single", graph=g, ids=[0], total=1, desc=g.name)
+    return dict(kind="single", graph=g, ids=[rank], total=1, desc=g.name)
 
 
 def union_of(parts):
@@ -186,8 +186,8 @@ def run_wbpr(args, rank, world, local_rank):
     bitmap_d = torch.empty((G.n + 31) // 32, dtype=torch.int32, device=dev)
     bitmap_h = torch.empty((G.n + 31) // 32, dtype=torch.int32).pin_memory()
     stream = torch.cuda.current_stream(dev)
-    rec = torch.zeros((k, 8), dtype=torch.int64, device=dev)
-    gathered = torch.zeros((k * world, 8), dtype=torch.int64, device=dev) if world > 1 else None
+    from paper_2404_00270_b200.batch import gather_records, make_records
+    gathered = None
 
     def step(host=False):
         if host:
@@ -196,18 +196,11 @@ def run_wbpr(args, rank, world, local_rank):
         else:
             flows, cuts, _, st = W.maxflow_batch(ro_d, col_d, cap_d, vbase, s, t, workspace=ws, bitmap=bitmap_d,
                                                  device=dev, **opt)
-        # 64-B result record per instance: id, status, F, cut, rounds, GRs, pushes, relabels
-        r = np.zeros((k, 8), np.int64)
-        r[:, 0] = wl["ids"]
-        r[:, 2] = flows
-        r[:, 3] = cuts
-        r[:, 4] = st["rounds"]
-        r[:, 5] = st["global_relabels"]
-        r[:, 6] = st["pushes"]
-        r[:, 7] = st["relabels"]
-        rec.copy_(torch.from_numpy(r), non_blocking=False)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, rec)   # the only collective: NCCL result gather
+        # 64-B result record per instance (id, status, F, cut, rounds, GRs, pushes, relabels),
+        # gathered over ranks: the only collective (NCCL all_gather)
+        nonlocal gathered
+        rec = torch.from_numpy(make_records(wl["ids"], flows, cuts, st)).to(dev)
+        gathered = gather_records(rec, wl["total"] if wl["kind"] == "batch" else world, world)
         return st, flows, cuts
 
     for _ in range(args.warmup):
@@ -254,9 +247,8 @@ def run_wbpr(args, rank, world, local_rank):
     if rank != 0:
         return None
     # certificate of every gathered record: F == cut capacity
-    if world > 1:
-        g = gathered.cpu().numpy()
-        assert np.all(g[:, 2] == g[:, 3]), "certificate failed in gathered records"
+    g = gathered.cpu().numpy()
+    assert np.all(g[:, 2] == g[:, 3]), "certificate failed in gathered records"
     assert np.all(flows == cuts)
     # roofline of the dominant kernel: the persistent solve kernel vs the build kernels
     hbm, peak_src = peaks()

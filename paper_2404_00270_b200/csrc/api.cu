@@ -116,8 +116,13 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
   a.cap0 = at<int>(W.base, L.regB + L.bcap0);
   a.rarc = at<int2>(W.base, L.regC + 8 * (size_t)L.m);
   a.bcf = at<int>(W.base, L.regB);
-  a.colv = at<int>(W.base, L.regA);
   a.vbase = d_vbase; a.k = k;
+  a.rsoff = at<int>(W.base, L.rsoff);
+  a.need = at<uint8_t>(W.base, L.deact);
+  a.q1 = at<int>(W.base, L.q1);
+  a.mtasks = at<int2>(W.base, L.hc0);
+  a.mheads = at<int>(W.base, L.hc1);
+  a.colv = at<int>(W.base, L.regA + 4 * (size_t)L.m);
 
   build_validate(a, st);
   CK(cudaGetLastError());
@@ -131,9 +136,10 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
     return fail(WBPR_EINVAL, "edge " + std::to_string(bad_edge) +
                                  " has a column outside its instance's range or a negative capacity");
   a.maxlen = c.maxlen;
+  a.maxlen_out = c.maxlen_out;
   if (layout == WBPR_LAYOUT_BCSR) {
     a.H = 2 * L.m - c.selfloops;
-    build_bcsr(a, st);
+    build_bcsr_merge(a, st);
     build_bcsr_mate(a, st);
     CK(cudaGetLastError());
     Mf = -1;   // on the device

@@ -34,13 +34,19 @@ __device__ __forceinline__ int row_of32(const int* __restrict__ off, int n, int 
 }
 
 // Row-offset sanity + raw out-degrees (self-loops included as sentinel slots).
-__global__ void k_rows(const int64_t* __restrict__ ro, int64_t n, int64_t m, int* deg, Ctrl* ctrl) {
+__global__ void k_rows(const int64_t* __restrict__ ro, int64_t n, int64_t m, int* deg, Ctrl* ctrl, int write_deg) {
+  int mx = 0;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
     int64_t a = ro[u], b = ro[u + 1];
     bool bad = a > b || a < 0 || b > m || (u == 0 && a != 0) || (u == n - 1 && b != m);
     if (bad) atomicExch(&ctrl->bad_rows, 1);
-    deg[u] = bad ? 0 : (int)(b - a);
+    int d = bad ? 0 : (int)(b - a);
+    if (write_deg) deg[u] = d;
+    mx = max(mx, d);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+  if (lane_id() == 0) atomicMax(&ctrl->maxlen_out, mx);
 }
 
 constexpr int kEdgesPerThread = 8;
@@ -265,7 +271,9 @@ static unsigned grid_exact(int64_t items, int threads) {
 // deg[] and fills ctrl->{bad_edge, bad_rows, selfloops, maxlen}.
 void build_validate(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
-  { k_rows<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.ro, a.n, a.m, a.deg, a.ctrl); note_launch(); }
+  // BCSR: deg[] = in-degrees (out-rows come straight from the input); RCSR: deg[] = out-degrees
+  if (a.layout == 0) cudaMemsetAsync(a.deg, 0, sizeof(int) * a.n, st);
+  { k_rows<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.ro, a.n, a.m, a.deg, a.ctrl, a.layout != 0); note_launch(); }
   int64_t threads = (a.m + kEdgesPerThread - 1) / kEdgesPerThread;
   if (a.m > 0)
     { k_edges<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, a.n, a.m, a.deg, a.ctrl,
@@ -302,6 +310,10 @@ void build_bcsr_mate(const BuildArgs& a, cudaStream_t st) {
   { k_colcopy<<<grid_for(a.H, T, a.num_sms, 32), T, 0, st>>>(a.arc, a.ctrl, a.colv); note_launch(); }
   int64_t threads = (a.H + kEdgesPerThread - 1) / kEdgesPerThread;
   if (a.H > 0) { k_mate<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.colv, (int)a.n, a.ctrl, a.mate, a.ctrl); note_launch(); }
+}
+
+void k_ro_to_i32_ext(const int64_t* ro, int64_t n, int* out, int num_sms, cudaStream_t st) {
+  { k_ro_to_i32<<<grid_for(n + 1, 256, num_sms), 256, 0, st>>>(ro, n, out); note_launch(); }
 }
 
 void build_rcsr_forward(const BuildArgs& a, cudaStream_t st) {

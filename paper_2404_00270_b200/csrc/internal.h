@@ -92,7 +92,9 @@ struct Ctrl {
   int hub_chunks;         // build scratch counter
   int sort_items;         // build scratch counter
   int sort_items_med;     // build scratch counter
-  int pad0[5];
+  int mlist_w, mlist_c;   // build: vertices merged by a warp / by a CTA
+  int maxlen_out;         // build: longest input row
+  int pad0[2];
   long long gap_level;    // online gap: lowest empty level seen this round (A6)
 };
 

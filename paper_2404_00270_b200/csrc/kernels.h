@@ -15,6 +15,12 @@ void exclusive_scan(int* a, int64_t N, int* part, cudaStream_t st);
 
 void segmented_sort(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl,
                     int2* items, int2* items_med, int* big, int num_sms, cudaStream_t st);
+void segmented_sort_filtered(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen,
+                             const uint8_t* need, Ctrl* ctrl, int2* items, int2* items_med, int* big, int num_sms,
+                             cudaStream_t st);
+void segmented_sort32(uint32_t* keys, uint32_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl, int2* items,
+                      int2* items_med, int* big, int num_sms, cudaStream_t st);
+void k_ro_to_i32_ext(const int64_t* ro, int64_t n, int* out, int num_sms, cudaStream_t st);
 
 struct BuildArgs {
   int64_t n, m, H;
@@ -42,11 +48,18 @@ struct BuildArgs {
   const int64_t* vbase;  // batch instance ranges (device), k entries + 1
   int k;
   int* colv;             // dense copy of the merged columns (region A after the merge)
+  int* rsoff;            // BCSR merge build: in-list offsets
+  uint8_t* need;         // BCSR merge build: per-row "not sorted" flags
+  int* q1;
+  int2* mtasks;          // BCSR merge build: chunk tasks of hub vertices
+  int* mheads;
+  int maxlen_out;
 };
 
 void build_validate(const BuildArgs& a, cudaStream_t st);
 void build_bcsr(const BuildArgs& a, cudaStream_t st);
 void build_bcsr_mate(const BuildArgs& a, cudaStream_t st);
+void build_bcsr_merge(const BuildArgs& a, cudaStream_t st);
 void build_rcsr_forward(const BuildArgs& a, cudaStream_t st);
 void build_rcsr_reverse_counts(const BuildArgs& a, int Mf, cudaStream_t st);
 void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st);

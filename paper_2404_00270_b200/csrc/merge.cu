@@ -1,0 +1,319 @@
+// merge.cu — BCSR construction (A1) by merging two sorted lists per vertex.
+//
+// seg(x) of the BCSR (§3.2) is the column-sorted union of x's
+// out-arcs (its input CSR row, cap c) and its in-arcs (the transposed edges,
+// residual capacity 0).  Instead of sorting the concatenation:
+//   * out-rows are taken in input order and sorted only where the input row is not
+//     already column-sorted (detected per row while the 64-bit keys are written);
+//   * in-lists carry 32-bit source ids only (their capacity is always 0), scattered
+//     by a histogram + atomic cursor and sorted with the 32-bit segmented sort;
+//   * a merge pass counts the distinct columns per vertex (parallel edges and
+//     antiparallel pairs collapse), a scan over n gives the final offsets,
+//     and a second merge pass writes {col, cf = sum of caps} and cap0.
+// Merge classes: <= 32 elements: one thread, sequential two-pointer merge;
+// <= 8192: one warp, merge path advanced 32 outputs at a time with the 32-element
+// windows of both lists held in registers (co-rank by shuffles); larger: split into
+// 4096-output warp tasks whose starts come from a global co-rank search.
+#include <climits>
+
+#include "internal.h"
+#include "kernels.h"
+
+namespace wbpr {
+
+constexpr uint64_t kSentKey = ~0ull;
+constexpr uint32_t kInf = 0xffffffffu;
+constexpr int kMergeThreadMax = 32;
+constexpr int kMergeWarpMax = 8192;
+constexpr int kMergeChunk = 4096;
+
+__device__ __forceinline__ uint32_t kcol(uint64_t k) { return (uint32_t)(k >> 32); }
+__device__ __forceinline__ long long kcap(uint64_t k) { return (long long)(uint32_t)(k & 0xffffffffu); }
+
+__device__ __forceinline__ int row_of64(const int64_t* __restrict__ ro, int64_t n, int64_t i) {
+  int64_t lo = 0, hi = n;
+  while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (__ldg(ro + mid) <= i) lo = mid; else hi = mid; }
+  return (int)lo;
+}
+
+// 64-bit out-keys in input order; rows that are not non-decreasing get need[u] = 1.
+__global__ void k_outkeys(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                          const int32_t* __restrict__ cap, int64_t n, int64_t m, uint64_t* keys, uint8_t* need) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i0 = t * 8;
+  if (i0 >= m) return;
+  int u = row_of64(ro, n, i0);
+  int64_t i1 = i0 + 8 < m ? i0 + 8 : m;
+  for (int64_t i = i0; i < i1; ++i) {
+    while (__ldg(ro + u + 1) <= i) ++u;
+    int v = col[i];
+    uint64_t k = (v == u) ? kSentKey : (((uint64_t)(uint32_t)v << 32) | (uint32_t)cap[i]);
+    keys[i] = k;
+    if (i > __ldg(ro + u)) {
+      int pv = col[i - 1];
+      uint64_t pk = (pv == u) ? kSentKey : (((uint64_t)(uint32_t)pv << 32) | (uint32_t)cap[i - 1]);
+      if (k < pk) need[u] = 1;
+    }
+  }
+}
+
+// in-list scatter: edge (u -> v), u != v, lands in v's list as the 32-bit id u.
+__global__ void k_inscatter(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n, int64_t m,
+                            const int* __restrict__ rsoff, int* cursor, uint32_t* inkeys) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t i0 = t * 8;
+  if (i0 >= m) return;
+  int u = row_of64(ro, n, i0);
+  int64_t i1 = i0 + 8 < m ? i0 + 8 : m;
+  for (int64_t i = i0; i < i1; ++i) {
+    while (__ldg(ro + u + 1) <= i) ++u;
+    int v = col[i];
+    if (v == u) continue;
+    int q = rsoff[v] + atomicAdd(cursor + v, 1);
+    inkeys[q] = (uint32_t)u;
+  }
+}
+
+struct MergeArgs {
+  const int* ooff;          // out-list offsets (int32 copy of row_offsets), n+1
+  const uint64_t* outk;     // sorted out keys (col << 32 | cap), self-loops = kSentKey (last)
+  const int* ioff;          // in-list offsets, n+1
+  const uint32_t* ink;      // sorted in-list source ids
+  int n;
+  int* mdeg;                // pass 0 output: distinct columns per vertex
+  const int* off;           // pass 1 input: final offsets
+  int2* arc;                // pass 1 output
+  int* cap0;
+  int* wlist;               // vertices for the warp class
+  int2* tasks;              // (vertex, chunk) tasks of the chunked class (> kMergeWarpMax)
+  int* chunk_heads;         // distinct columns found by each chunk task
+  Ctrl* ctrl;
+};
+
+__device__ __forceinline__ void emit(const MergeArgs& a, int slot, uint32_t c, long long sum) {
+  if (sum > INT_MAX) { atomicExch(&a.ctrl->overflow, 1); sum = INT_MAX; }
+  a.arc[slot] = make_int2((int)c, (int)sum);
+  a.cap0[slot] = (int)sum;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
+  const int lane = lane_id();
+  for (int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < a.n; base += gridDim.x * blockDim.x) {
+    int x = base + lane;
+    int ob = 0, lo = 0, ib = 0, li = 0;
+    if (x < a.n) {
+      ob = __ldg(a.ooff + x); lo = __ldg(a.ooff + x + 1) - ob;
+      ib = __ldg(a.ioff + x); li = __ldg(a.ioff + x + 1) - ib;
+    }
+    bool big = x < a.n && lo + li > kMergeThreadMax;
+    if (PASS == 0) {
+      bool wl = big && lo + li <= kMergeWarpMax, cl = big && !wl;
+      unsigned bw = __ballot_sync(FULL, wl);
+      int pw = 0;
+      if (lane == 0 && bw) pw = atomicAdd(&a.ctrl->mlist_w, __popc(bw));
+      pw = __shfl_sync(FULL, pw, 0);
+      unsigned lt = (1u << lane) - 1u;
+      if (wl) a.wlist[pw + __popc(bw & lt)] = x;
+      if (cl) {   // split into kMergeChunk-output tasks (rare: hubs)
+        int nch = (lo + li + kMergeChunk - 1) / kMergeChunk;
+        int t0 = atomicAdd(&a.ctrl->mlist_c, nch);
+        for (int c = 0; c < nch; ++c) a.tasks[t0 + c] = make_int2(x, c);
+        a.mdeg[x] = 0;
+      }
+    }
+    if (x >= a.n || big) continue;
+    int i = 0, j = 0, r = 0;
+    int slot0 = PASS == 1 ? __ldg(a.off + x) : 0;
+    while (true) {
+      uint32_t co = i < lo ? kcol(a.outk[ob + i]) : kInf;
+      uint32_t ci = j < li ? a.ink[ib + j] : kInf;
+      uint32_t c = co < ci ? co : ci;
+      if (c == kInf) break;
+      long long sum = 0;
+      while (i < lo) {
+        uint64_t k = a.outk[ob + i];
+        if (kcol(k) != c) break;
+        sum += kcap(k);
+        ++i;
+      }
+      while (j < li && a.ink[ib + j] == c) ++j;
+      if (PASS == 1) emit(a, slot0 + r, c, sum);
+      ++r;
+    }
+    if (PASS == 0) a.mdeg[x] = r;
+  }
+}
+
+// One warp walks output positions [k0, k1) of the merge of Out (lo) and In (li),
+// starting at list positions (i0, j0) with the previous output column prev.
+// PASS 0: returns the number of distinct-column heads; PASS 1: also writes them at
+// slot base + rank.
+template <int PASS>
+__device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int lo, int ib, int li, int i0, int j0,
+                                                int k0, int k1, uint32_t prev, int slot_base) {
+  const int lane = lane_id();
+  int heads = 0;
+  for (int produced = k0; produced < k1; produced += 32) {
+    uint32_t av = (i0 + lane < lo) ? kcol(a.outk[ob + i0 + lane]) : kInf;
+    uint32_t bv = (j0 + lane < li) ? a.ink[ib + j0 + lane] : kInf;
+    int la = lo - i0 < 32 ? lo - i0 : 32;
+    int lb = li - j0 < 32 ? li - j0 : 32;
+    if (la < 0) la = 0;
+    if (lb < 0) lb = 0;
+    // co-rank of output k = lane inside the two register windows (A wins ties)
+    int k = lane;
+    int rlo = k - lb > 0 ? k - lb : 0, rhi = k < la ? k : la;
+#pragma unroll
+    for (int it = 0; it < 6; ++it) {
+      int mid = (rlo + rhi) >> 1;
+      int bidx = k - mid - 1;
+      uint32_t Am = __shfl_sync(FULL, av, mid & 31);
+      uint32_t Bm = __shfl_sync(FULL, bv, (bidx < 0 ? 0 : bidx) & 31);
+      if (rlo < rhi) {
+        if (Am <= Bm) rlo = mid + 1; else rhi = mid;
+      }
+    }
+    int i = rlo, j = k - rlo;
+    uint32_t Ai = __shfl_sync(FULL, av, i & 31);
+    uint32_t Bj = __shfl_sync(FULL, bv, j & 31);
+    bool takeA = j >= lb || (i < la && Ai <= Bj);
+    uint32_t c = takeA ? Ai : Bj;
+    bool valid = produced + lane < k1 && c != kInf;
+    uint32_t pc = __shfl_up_sync(FULL, c, 1);
+    if (lane == 0) pc = prev;
+    bool head = valid && c != pc;
+    unsigned hm = __ballot_sync(FULL, head);
+    if (PASS == 1 && head) {
+      long long sum = 0;
+      if (takeA) {
+        for (int q = i0 + i; q < lo; ++q) {
+          uint64_t kk = a.outk[ob + q];
+          if (kcol(kk) != c) break;
+          sum += kcap(kk);
+        }
+      }
+      emit(a, slot_base + heads + __popc(hm & ((1u << lane) - 1u)), c, sum);
+    }
+    heads += __popc(hm);
+    int nA = __shfl_sync(FULL, i + (takeA ? 1 : 0), 31);
+    prev = __shfl_sync(FULL, c, 31);
+    i0 += nA;
+    j0 += 32 - nA;
+  }
+  return heads;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(256) k_merge_warp(MergeArgs a) {
+  const int cnt = a.ctrl->mlist_w;
+  const int lane = lane_id();
+  int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int it = wg; it < cnt; it += nw) {
+    int x = a.wlist[it];
+    int ob = __ldg(a.ooff + x), lo = __ldg(a.ooff + x + 1) - ob;
+    int ib = __ldg(a.ioff + x), li = __ldg(a.ioff + x + 1) - ib;
+    int base = PASS == 1 ? __ldg(a.off + x) : 0;
+    int h = warp_merge_range<PASS>(a, ob, lo, ib, li, 0, 0, 0, lo + li, kInf, base);
+    if (PASS == 0 && lane == 0) a.mdeg[x] = h;
+  }
+}
+
+// global co-rank on the full lists (Out compared by column)
+__device__ __forceinline__ int co_rank_lists(int k, const uint64_t* A, int la, const uint32_t* B, int lb) {
+  int lo = k - lb > 0 ? k - lb : 0, hi = k < la ? k : la;
+  while (lo < hi) {
+    int i = (lo + hi) >> 1;
+    if (kcol(A[i]) <= B[k - i - 1]) lo = i + 1; else hi = i;
+  }
+  return lo;
+}
+
+// Chunked class: one warp per (vertex, chunk) task of kMergeChunk outputs; the
+// chunk's start in both lists is found by a global co-rank search.
+template <int PASS>
+__global__ void __launch_bounds__(256) k_merge_chunk(MergeArgs a) {
+  const int cnt = a.ctrl->mlist_c;
+  const int lane = lane_id();
+  int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = wg; t < cnt; t += nw) {
+    int2 tk = a.tasks[t];
+    int x = tk.x, c = tk.y;
+    int ob = __ldg(a.ooff + x), lo = __ldg(a.ooff + x + 1) - ob;
+    int ib = __ldg(a.ioff + x), li = __ldg(a.ioff + x + 1) - ib;
+    int total = lo + li;
+    int k0 = c * kMergeChunk;
+    int k1 = k0 + kMergeChunk < total ? k0 + kMergeChunk : total;
+    int i0 = co_rank_lists(k0, a.outk + ob, lo, a.ink + ib, li);
+    int j0 = k0 - i0;
+    uint32_t prev = kInf;
+    if (k0 > 0) {
+      uint32_t pa = i0 > 0 ? kcol(a.outk[ob + i0 - 1]) : 0u;
+      uint32_t pb = j0 > 0 ? a.ink[ib + j0 - 1] : 0u;
+      prev = pa > pb ? pa : pb;
+    }
+    if (PASS == 0) {
+      int h = warp_merge_range<0>(a, ob, lo, ib, li, i0, j0, k0, k1, prev, 0);
+      if (lane == 0) {
+        a.chunk_heads[t] = h;
+        atomicAdd(a.mdeg + x, h);
+      }
+    } else {
+      int before = 0;
+      for (int q = lane; q < c; q += 32) before += a.chunk_heads[t - c + q];
+      before = warp_sum(before);
+      warp_merge_range<1>(a, ob, lo, ib, li, i0, j0, k0, k1, prev, __ldg(a.off + x) + before);
+    }
+  }
+}
+
+static unsigned gridcap(int64_t items, int threads, int num_sms, int per_sm) {
+  int64_t b = (items + threads - 1) / threads;
+  if (b > (int64_t)num_sms * per_sm) b = (int64_t)num_sms * per_sm;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+// Build BCSR from the validated input (BuildArgs: deg = in-degrees, maxlen = max
+// in-degree, maxlen_out = max out-degree).
+void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
+  const int T = 256;
+  const int64_t n = a.n, m = a.m;
+  // in-list offsets; out-list offsets (int32 copy of the input row offsets)
+  cudaMemcpyAsync(a.rsoff, a.deg, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
+  exclusive_scan(a.rsoff, n, a.scan_part, st);
+  { k_ro_to_i32_ext(a.ro, n, a.soff, a.num_sms, st); }
+  uint64_t* outk = a.tmp;                                     // region B [0, 8m)
+  uint32_t* ink = reinterpret_cast<uint32_t*>(a.keys);        // region A [0, 4m)
+  uint32_t* itmp = ink + m;                                   // region A [4m, 8m)
+  uint64_t* otmp = reinterpret_cast<uint64_t*>(a.arc);        // region C [0, 8m)
+  int2* items = a.arc + m;                                    // region C [8m, 12m)
+  int2* items_med = a.arc + m + m / 2 + 1;                    // region C [12m, 16m)
+  cudaMemsetAsync(a.need, 0, n, st);
+  cudaMemsetAsync(a.cursor, 0, sizeof(int) * n, st);
+  int64_t threads = (m + 7) / 8;
+  if (m > 0) {
+    { k_outkeys<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, outk, a.need); note_launch(); }
+    { k_inscatter<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(a.ro, a.col, n, m, a.rsoff, a.cursor, ink); note_launch(); }
+  }
+  segmented_sort_filtered(outk, otmp, a.soff, (int)n, a.maxlen_out, a.need, a.ctrl, items, items_med, a.q0,
+                          a.num_sms, st);
+  segmented_sort32(ink, itmp, a.rsoff, (int)n, a.maxlen, a.ctrl, items, items_med, a.q0, a.num_sms, st);
+  MergeArgs ma;
+  ma.ooff = a.soff; ma.outk = outk; ma.ioff = a.rsoff; ma.ink = ink; ma.n = (int)n;
+  ma.mdeg = a.deg; ma.off = a.off; ma.arc = a.arc; ma.cap0 = a.cap0;
+  ma.wlist = a.q0; ma.tasks = a.mtasks; ma.chunk_heads = a.mheads; ma.ctrl = a.ctrl;
+  cudaMemsetAsync(&a.ctrl->mlist_w, 0, 2 * sizeof(int), st);
+  { k_merge_thread<0><<<gridcap(n, T, a.num_sms, 16), T, 0, st>>>(ma); note_launch(); }
+  { k_merge_warp<0><<<a.num_sms * 16, T, 0, st>>>(ma); note_launch(); }
+  { k_merge_chunk<0><<<a.num_sms * 4, T, 0, st>>>(ma); note_launch(); }
+  cudaMemcpyAsync(a.off, a.deg, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
+  exclusive_scan(a.off, n, a.scan_part, st);
+  cudaMemcpyAsync(&a.ctrl->M, a.off + n, sizeof(int), cudaMemcpyDeviceToDevice, st);
+  { k_merge_thread<1><<<gridcap(n, T, a.num_sms, 16), T, 0, st>>>(ma); note_launch(); }
+  { k_merge_warp<1><<<a.num_sms * 16, T, 0, st>>>(ma); note_launch(); }
+  { k_merge_chunk<1><<<a.num_sms * 4, T, 0, st>>>(ma); note_launch(); }
+}
+
+}  // namespace wbpr

@@ -1,36 +1,45 @@
-// segsort.cu — hand-written segmented sort of 64-bit keys for residual
+// segsort.cu — hand-written segmented sort (32- or 64-bit keys) for residual
 // construction (A1).  BCSR needs every vertex segment sorted by column (PAPER.md
 // §3.2, "sort the column list in ascending order by vertex ID") so that
 // duplicate columns become adjacent (merge) and the reverse arc can be located
 // by binary search once, into mate[].
 //
 // Segment classes (lengths from 1 to ~1.6e5 at R-MAT scale 22):
-//   len <= 32        one warp per segment, rank sort in registers (32 shuffles)
-//   32 < len <= 256  one warp per segment, register bitonic sort (8 keys per lane,
-//                    shuffles for the cross-lane stages, no shared memory / barriers)
-//   256 < len <= 4096 one CTA per segment, bitonic sort in shared memory
-//   len > 4096       4096-key chunks sorted as above, then log2(len/4096)
-//                    merge passes (merge-path co-rank, 8 outputs per thread),
-//                    ping-ponging between keys and tmp.
+//   len <= 32         one warp per segment, rank sort in registers (32 shuffles)
+//   32 < len <= 256   one warp per segment, register bitonic network sized to the
+//                     length (2/4/8 keys per lane; shuffles for the cross-lane stages,
+//                     no shared memory, no barriers)
+//   256 < len <= 4096 one 512-thread CTA: each warp sorts a 256-key chunk in
+//                     registers, then merge-path passes in shared memory
+//   len > 4096        4096-key chunks sorted as above, then log2(len/4096) merge
+//                     passes in global memory (co-rank search, 8 outputs per thread),
+//                     ping-ponging between keys and tmp.
+// An optional per-segment `need` flag skips segments known to be sorted already.
 #include "internal.h"
 #include "kernels.h"
 
 namespace wbpr {
 
 constexpr int kTileThreads = 512;
+constexpr int kMedLen = 256;   // warp register sort up to this length
 
-__global__ void __launch_bounds__(256) k_sort_warp(uint64_t* keys, const int* __restrict__ off, int nseg) {
+template <typename K> __device__ __forceinline__ K key_max() { return (K)~(K)0; }
+
+template <typename K>
+__global__ void __launch_bounds__(256) k_sort_warp(K* keys, const int* __restrict__ off, int nseg,
+                                                   const uint8_t* __restrict__ need) {
   int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = lane_id();
   int nw = (gridDim.x * blockDim.x) >> 5;
   for (int sgi = wg; sgi < nseg; sgi += nw) {
+    if (need && !need[sgi]) continue;
     int beg = off[sgi], len = off[sgi + 1] - beg;
     if (len < 2 || len > 32) continue;
-    uint64_t k = lane < len ? keys[beg + lane] : ~0ull;
+    K k = lane < len ? keys[beg + lane] : key_max<K>();
     int rank = 0;
 #pragma unroll 8
     for (int j = 0; j < 32; ++j) {
-      uint64_t o = __shfl_sync(FULL, k, j);
+      K o = __shfl_sync(FULL, k, j);
       rank += (o < k) || (o == k && j < lane);
     }
     __syncwarp();
@@ -38,13 +47,9 @@ __global__ void __launch_bounds__(256) k_sort_warp(uint64_t* keys, const int* __
   }
 }
 
-constexpr int kMedLen = 256;   // warp register sort up to this length
-
-// Bitonic network over P = 32*NR keys held by one warp as r[j] = element j*32 + lane:
-// stages with partner distance >= 32 swap registers inside a lane, shorter ones
-// exchange with __shfl_xor_sync.  No shared memory, no barriers.
-template <int NR>
-__device__ __forceinline__ void warp_bitonic(uint64_t (&r)[NR], int lane) {
+// Bitonic network over P = 32*NR keys held by one warp as r[j] = element j*32 + lane.
+template <typename K, int NR>
+__device__ __forceinline__ void warp_bitonic(K (&r)[NR], int lane) {
   constexpr int P = 32 * NR;
 #pragma unroll
   for (int k = 2; k <= P; k <<= 1) {
@@ -56,7 +61,7 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&r)[NR], int lane) {
         for (int j = 0; j < NR; ++j) {
           if ((j & dj) == 0) {
             const bool up = ((j * 32 + lane) & k) == 0;
-            uint64_t a = r[j], b = r[j | dj];
+            K a = r[j], b = r[j | dj];
             if ((a > b) == up) { r[j] = b; r[j | dj] = a; }
           }
         }
@@ -64,9 +69,9 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&r)[NR], int lane) {
         const bool lower = (lane & jj) == 0;
 #pragma unroll
         for (int j = 0; j < NR; ++j) {
-          uint64_t o = __shfl_xor_sync(FULL, r[j], jj);
+          K o = __shfl_xor_sync(FULL, r[j], jj);
           const bool up = ((j * 32 + lane) & k) == 0;
-          uint64_t mn = r[j] < o ? r[j] : o, mx = r[j] < o ? o : r[j];
+          K mn = r[j] < o ? r[j] : o, mx = r[j] < o ? o : r[j];
           r[j] = (lower == up) ? mn : mx;
         }
       }
@@ -74,15 +79,15 @@ __device__ __forceinline__ void warp_bitonic(uint64_t (&r)[NR], int lane) {
   }
 }
 
-template <int NR>
-__device__ __forceinline__ void warp_sort_segment(uint64_t* keys, int beg, int len, int lane) {
-  uint64_t r[NR];
+template <typename K, int NR>
+__device__ __forceinline__ void warp_sort_segment(K* keys, int beg, int len, int lane) {
+  K r[NR];
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     int e = j * 32 + lane;
-    r[j] = e < len ? keys[beg + e] : ~0ull;
+    r[j] = e < len ? keys[beg + e] : key_max<K>();
   }
-  warp_bitonic<NR>(r, lane);
+  warp_bitonic<K, NR>(r, lane);
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     int e = j * 32 + lane;
@@ -90,26 +95,26 @@ __device__ __forceinline__ void warp_sort_segment(uint64_t* keys, int beg, int l
   }
 }
 
-// 32 < len <= 256: one warp per segment; network size adapted to the length.
-__global__ void __launch_bounds__(256) k_sort_med(uint64_t* keys, const int2* __restrict__ items,
-                                                  const Ctrl* ctrl) {
-  const int nitems = ctrl->sort_items_med;
+template <typename K>
+__global__ void __launch_bounds__(256) k_sort_med(K* keys, const int2* __restrict__ items, const int* count) {
+  const int nitems = *count;
   int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nw = (gridDim.x * blockDim.x) >> 5;
   int lane = lane_id();
   for (int it = wg; it < nitems; it += nw) {
     int2 item = items[it];
-    if (item.y <= 64) warp_sort_segment<2>(keys, item.x, item.y, lane);
-    else if (item.y <= 128) warp_sort_segment<4>(keys, item.x, item.y, lane);
-    else warp_sort_segment<8>(keys, item.x, item.y, lane);
+    if (item.y <= 64) warp_sort_segment<K, 2>(keys, item.x, item.y, lane);
+    else if (item.y <= 128) warp_sort_segment<K, 4>(keys, item.x, item.y, lane);
+    else warp_sort_segment<K, 8>(keys, item.x, item.y, lane);
   }
 }
 
 // Enumerate sort items: 32 < len <= 256 -> warp items; 256 < len <= tile -> CTA item;
 // longer segments -> ceil(len/tile) CTA chunk items and the `big` list.
-__global__ void k_sort_items(const int* __restrict__ off, int nseg, int2* items, int2* items_med, int* big,
-                             Ctrl* ctrl) {
+__global__ void k_sort_items(const int* __restrict__ off, int nseg, const uint8_t* __restrict__ need,
+                             int2* items, int2* items_med, int* big, Ctrl* ctrl) {
   for (int sgi = blockIdx.x * blockDim.x + threadIdx.x; sgi < nseg; sgi += gridDim.x * blockDim.x) {
+    if (need && !need[sgi]) continue;
     int beg = off[sgi], len = off[sgi + 1] - beg;
     if (len <= 32) continue;
     if (len <= kMedLen) {
@@ -129,56 +134,53 @@ __global__ void k_sort_items(const int* __restrict__ off, int nseg, int2* items,
 
 // Smallest i in [max(0,k-lb), min(k,la)] with A[i] > B[k-i-1] (A wins ties): the
 // number of outputs among the first k that come from A.
-__device__ __forceinline__ int co_rank(int k, const uint64_t* A, int la, const uint64_t* B, int lb) {
+template <typename K>
+__device__ __forceinline__ int co_rank(int k, const K* A, int la, const K* B, int lb) {
   int lo = k - lb > 0 ? k - lb : 0, hi = k < la ? k : la;
   while (lo < hi) {
-    int i = (lo + hi) >> 1;          // candidate: i from A, k-i from B
-    // too few from A if A[i] <= B[k-i-1]
+    int i = (lo + hi) >> 1;
     if (A[i] <= B[k - i - 1]) lo = i + 1; else hi = i;
   }
   return lo;
 }
 
-// 256 < len <= 4096 (and 4096-key chunks of longer segments): one 512-thread CTA.
-// Each warp sorts a 256-key chunk in registers (warp_bitonic), then log2(chunks)
-// merge-path passes in shared memory (8 outputs per thread, co-rank search).
-constexpr int kCtaSmemBytes = 2 * kSortTile * 8;   // ping-pong buffers (64 KB)
-__global__ void __launch_bounds__(kTileThreads) k_sort_tile(uint64_t* keys, const int2* __restrict__ items,
-                                                             const Ctrl* ctrl) {
-  extern __shared__ uint64_t sm[];
-  uint64_t* A = sm;
-  uint64_t* B = sm + kSortTile;
-  const int nitems = ctrl->sort_items;
+template <typename K>
+__global__ void __launch_bounds__(kTileThreads) k_sort_tile(K* keys, const int2* __restrict__ items,
+                                                             const int* count) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  K* A = reinterpret_cast<K*>(smraw);
+  K* B = A + kSortTile;
+  const int nitems = *count;
   const int lane = lane_id(), w = warp_id();
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     int2 item = items[it];
     const int beg = item.x, len = item.y;
     const int nc = (len + kMedLen - 1) / kMedLen;          // 256-key chunks
     if (w < nc) {
-      uint64_t r[8];
+      K r[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         int e = w * kMedLen + j * 32 + lane;
-        r[j] = e < len ? keys[beg + e] : ~0ull;
+        r[j] = e < len ? keys[beg + e] : key_max<K>();
       }
-      warp_bitonic<8>(r, lane);
+      warp_bitonic<K, 8>(r, lane);
 #pragma unroll
       for (int j = 0; j < 8; ++j) A[w * kMedLen + j * 32 + lane] = r[j];
     }
     __syncthreads();
     const int total = nc * kMedLen;
-    uint64_t* src = A;
-    uint64_t* dst = B;
+    K* src = A;
+    K* dst = B;
     for (int wd = kMedLen; wd < total; wd <<= 1) {
       for (int kk = threadIdx.x * 8; kk < total; kk += blockDim.x * 8) {
         int pair0 = kk / (2 * wd) * (2 * wd);
         int la = min(wd, total - pair0);
         int lb = min(wd, total - pair0 - la);
         if (lb < 0) lb = 0;
-        const uint64_t* SA = src + pair0;
-        const uint64_t* SB = SA + la;
+        const K* SA = src + pair0;
+        const K* SB = SA + la;
         int k = kk - pair0;
-        int i = co_rank(k, SA, la, SB, lb);
+        int i = co_rank<K>(k, SA, la, SB, lb);
         int j = k - i;
         int outn = min(8, la + lb - k);
         for (int q = 0; q < outn; ++q) {
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tile(uint64_t* keys, cons
         }
       }
       __syncthreads();
-      uint64_t* t = src; src = dst; dst = t;
+      K* t = src; src = dst; dst = t;
     }
     for (int i = threadIdx.x; i < len; i += blockDim.x) keys[beg + i] = src[i];
     __syncthreads();
@@ -195,27 +197,27 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tile(uint64_t* keys, cons
 }
 
 // One merge pass of width w over every big segment (one CTA per segment).
-__global__ void __launch_bounds__(256) k_merge_pass(const uint64_t* __restrict__ src, uint64_t* dst,
-                                                    const int* __restrict__ off, const int* __restrict__ big,
-                                                    const Ctrl* ctrl, int w) {
-  int nbig = ctrl->hub_chunks;
+template <typename K>
+__global__ void __launch_bounds__(256) k_merge_pass(const K* __restrict__ src, K* dst, const int* __restrict__ off,
+                                                    const int* __restrict__ big, const int* count, int w) {
+  int nbig = *count;
   for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
     int sgi = big[bi];
     int beg = off[sgi], len = off[sgi + 1] - beg;
     int ntask = (len + 7) >> 3;
     for (int tk = threadIdx.x; tk < ntask; tk += blockDim.x) {
-      int kk = tk << 3;                       // local output index
-      int pair0 = kk / (2 * w) * (2 * w);     // start of the pair of runs
+      int kk = tk << 3;
+      int pair0 = kk / (2 * w) * (2 * w);
       int la = min(w, len - pair0);
       int lb = min(w, len - pair0 - la);
       if (lb < 0) lb = 0;
-      const uint64_t* A = src + beg + pair0;
-      const uint64_t* B = A + la;
+      const K* A = src + beg + pair0;
+      const K* B = A + la;
       int k = kk - pair0;
-      int i = co_rank(k, A, la, B, lb);
+      int i = co_rank<K>(k, A, la, B, lb);
       int j = k - i;
       int outn = min(8, la + lb - k);
-      uint64_t* O = dst + beg + kk;
+      K* O = dst + beg + kk;
       for (int q = 0; q < outn; ++q) {
         bool takeA = j >= lb || (i < la && A[i] <= B[j]);
         O[q] = takeA ? A[i++] : B[j++];
@@ -224,10 +226,10 @@ __global__ void __launch_bounds__(256) k_merge_pass(const uint64_t* __restrict__
   }
 }
 
-__global__ void __launch_bounds__(256) k_copy_big(const uint64_t* __restrict__ src, uint64_t* dst,
-                                                  const int* __restrict__ off, const int* __restrict__ big,
-                                                  const Ctrl* ctrl) {
-  int nbig = ctrl->hub_chunks;
+template <typename K>
+__global__ void __launch_bounds__(256) k_copy_big(const K* __restrict__ src, K* dst, const int* __restrict__ off,
+                                                  const int* __restrict__ big, const int* count) {
+  int nbig = *count;
   for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
     int sgi = big[bi];
     int beg = off[sgi], len = off[sgi + 1] - beg;
@@ -235,39 +237,57 @@ __global__ void __launch_bounds__(256) k_copy_big(const uint64_t* __restrict__ s
   }
 }
 
-void segmented_sort(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl,
-                    int2* items, int2* items_med, int* big, int num_sms, cudaStream_t st) {
+template <typename K>
+void segmented_sort_t(K* keys, K* tmp, const int* off, int nseg, int maxlen, const uint8_t* need, Ctrl* ctrl,
+                      int2* items, int2* items_med, int* big, int num_sms, cudaStream_t st) {
   if (nseg <= 0 || maxlen < 2) return;
   cudaMemsetAsync(&ctrl->sort_items, 0, sizeof(int), st);
   cudaMemsetAsync(&ctrl->sort_items_med, 0, sizeof(int), st);
   cudaMemsetAsync(&ctrl->hub_chunks, 0, sizeof(int), st);
   {
-    int64_t warps = nseg;
-    int64_t blocks = (warps * 32 + 255) / 256;
+    int64_t blocks = ((int64_t)nseg * 32 + 255) / 256;
     if (blocks > (int64_t)num_sms * 64) blocks = (int64_t)num_sms * 64;
-    { k_sort_warp<<<(unsigned)blocks, 256, 0, st>>>(keys, off, nseg); note_launch(); }
+    { k_sort_warp<K><<<(unsigned)blocks, 256, 0, st>>>(keys, off, nseg, need); note_launch(); }
   }
   if (maxlen <= 32) return;
   {
     int64_t blocks = (nseg + 255) / 256;
     if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
-    { k_sort_items<<<(unsigned)blocks, 256, 0, st>>>(off, nseg, items, items_med, big, ctrl); note_launch(); }
+    { k_sort_items<<<(unsigned)blocks, 256, 0, st>>>(off, nseg, need, items, items_med, big, ctrl); note_launch(); }
   }
-  { k_sort_med<<<num_sms * 16, 256, 0, st>>>(keys, items_med, ctrl); note_launch(); }
+  { k_sort_med<K><<<num_sms * 16, 256, 0, st>>>(keys, items_med, &ctrl->sort_items_med); note_launch(); }
   if (maxlen <= kMedLen) return;
   {
-    cudaFuncSetAttribute(k_sort_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaSmemBytes);
-    k_sort_tile<<<num_sms * 3, kTileThreads, kCtaSmemBytes, st>>>(keys, items, ctrl); note_launch(); }
+    const int smem = 2 * kSortTile * (int)sizeof(K);
+    cudaFuncSetAttribute(k_sort_tile<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int per_sm = sizeof(K) == 8 ? 3 : 6;
+    k_sort_tile<K><<<num_sms * per_sm, kTileThreads, smem, st>>>(keys, items, &ctrl->sort_items);
+    note_launch();
+  }
   if (maxlen <= kSortTile) return;
-  const uint64_t* src = keys;
-  uint64_t* dst = tmp;
+  const K* src = keys;
+  K* dst = tmp;
   int passes = 0;
   for (int w = kSortTile; w < maxlen; w <<= 1) {
-    { k_merge_pass<<<num_sms * 8, 256, 0, st>>>(src, dst, off, big, ctrl, w); note_launch(); }
-    const uint64_t* t = src; src = dst; dst = const_cast<uint64_t*>(t);
+    { k_merge_pass<K><<<num_sms * 8, 256, 0, st>>>(src, dst, off, big, &ctrl->hub_chunks, w); note_launch(); }
+    const K* t = src; src = dst; dst = const_cast<K*>(t);
     ++passes;
   }
-  if (passes & 1) { k_copy_big<<<num_sms * 8, 256, 0, st>>>(tmp, keys, off, big, ctrl); note_launch(); }
+  if (passes & 1) { k_copy_big<K><<<num_sms * 8, 256, 0, st>>>(tmp, keys, off, big, &ctrl->hub_chunks); note_launch(); }
+}
+
+void segmented_sort(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl,
+                    int2* items, int2* items_med, int* big, int num_sms, cudaStream_t st) {
+  segmented_sort_t<uint64_t>(keys, tmp, off, nseg, maxlen, nullptr, ctrl, items, items_med, big, num_sms, st);
+}
+void segmented_sort_filtered(uint64_t* keys, uint64_t* tmp, const int* off, int nseg, int maxlen,
+                             const uint8_t* need, Ctrl* ctrl, int2* items, int2* items_med, int* big, int num_sms,
+                             cudaStream_t st) {
+  segmented_sort_t<uint64_t>(keys, tmp, off, nseg, maxlen, need, ctrl, items, items_med, big, num_sms, st);
+}
+void segmented_sort32(uint32_t* keys, uint32_t* tmp, const int* off, int nseg, int maxlen, Ctrl* ctrl, int2* items,
+                      int2* items_med, int* big, int num_sms, cudaStream_t st) {
+  segmented_sort_t<uint32_t>(keys, tmp, off, nseg, maxlen, nullptr, ctrl, items, items_med, big, num_sms, st);
 }
 
 }  // namespace wbpr

@@ -30,7 +30,8 @@ def _build(g, layout):
     return W.build_residual(ro, col, cap, layout=layout)
 
 
-BUILD_CASES = [("tiny", s) for s in range(12)] + [("c1", 1), ("grid", 1), ("rmat", 3), ("hubs", 0)]
+BUILD_CASES = [("tiny", s) for s in range(12)] + [("c1", 1), ("grid", 1), ("rmat", 3), ("hubs", 0),
+                                                  ("sorted_rmat", 4), ("bip", 1)]
 
 
 def _build_graph(kind, seed):
@@ -46,10 +47,19 @@ def _build_graph(kind, seed):
         # segments of every size class: <=32, <=4096, > 4096 (merge passes), duplicates
         rng = np.random.default_rng(7)
         n = 20000
-        src = np.concatenate([np.zeros(9000, np.int64), np.full(5000, 1), rng.integers(0, n, 30000), [5, 5, 5]])
-        dst = np.concatenate([rng.integers(0, n, 9000), rng.integers(0, n, 5000), rng.integers(0, n, 30000), [5, 6, 6]])
+        # vertex 2: > 8192 in-arcs (chunked merge), some parallel; vertex 0: 9000 unsorted out-arcs
+        src = np.concatenate([np.zeros(9000, np.int64), np.full(5000, 1), rng.integers(0, n, 30000), [5, 5, 5],
+                              rng.integers(3, n, 12000)])
+        dst = np.concatenate([rng.integers(0, n, 9000), rng.integers(0, n, 5000), rng.integers(0, n, 30000), [5, 6, 6],
+                              np.full(12000, 2)])
         cap = rng.integers(0, 50, src.shape[0]).astype(np.int32)
         return synth.shuffle_rows(synth.from_edges(n, src, dst, cap, 0, n - 1), 3)
+    if kind == "sorted_rmat":   # rows already column-sorted (no out-row sort needed)
+        return synth.rmat(12, 16, seed, "paper")
+    if kind == "bip":           # 2^12 x 2^12 matching network: s and t are hubs
+        l, r = synth.bipartite_edges(1 << 13, 1 << 13, 1 << 15, seed)
+        n, src, dst, cap, s, t = matching.network(1 << 13, 1 << 13, l, r)
+        return synth.shuffle_rows(synth.from_edges(n, src, dst, cap, s, t), seed)
     raise ValueError(kind)
 
 
