@@ -94,7 +94,8 @@ struct Ctrl {
   int sort_items_med;     // build scratch counter
   int mlist_w, mlist_c;   // build: vertices merged by a warp / by a CTA
   int maxlen_out;         // build: longest input row
-  int pad0[2];
+  int nhs;                // solve: entries of the static huge-chunk list
+  int pad0[1];
   long long gap_level;    // online gap: lowest empty level seen this round (A6)
 };
 
@@ -105,7 +106,7 @@ struct Layout {
   size_t ctrl, inst_s, inst_t, inst_flow, inst_cut, vbase;
   size_t in_row, in_col, in_cap;           // staging copy of a host CSR
   size_t h, e, term, deact, deg, cursor, off, soff, roff, rsoff;
-  size_t q0, q1, hq0, hq1, hc0, hc1, hist;
+  size_t q0, q1, hq0, hq1, hc0, hc1, hist, hs;
   size_t scan_part;
   size_t regA, regB, regC;                 // build / residual regions
   size_t bcap0;                            // offset inside regB of cap0
@@ -133,6 +134,7 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout) {
   L.hq0 = take(sizeof(HugeRec) * hub); L.hq1 = take(sizeof(HugeRec) * hub);
   L.hc0 = take(8 * (2 * hub + 64)); L.hc1 = take(8 * (2 * hub + 64));
   L.hist = take(4 * (n + 2));
+  L.hs = take(8 * (2 * hub + 64));
   L.scan_part = take(4 * ((H + 2 + n) / kScanTile + 64));
   L.regA = take(8 * H + 8);
   L.regB = take(8 * H + 1024);
@@ -163,6 +165,7 @@ struct SolveParams {
   HugeRec* hq[2];
   int2* hc[2];
   int* hist;
+  int2* hs;              // static (vertex, chunk) list of all vertices with > kChunk slots
   const long long* src; // sources [k]
   const long long* snk; // sinks [k]
   long long max_rounds;

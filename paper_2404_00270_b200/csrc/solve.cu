@@ -321,6 +321,13 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
     st_cg(P.e + v, 0ll);
     P.deact[v] = 0;
+    // static chunk list of the vertices with > kChunk slots (bottom-up BFS splits them)
+    int dg = ops.degree(v);
+    if (dg > kChunk) {
+      int nch = (dg + kChunk - 1) / kChunk;
+      int t0 = atomicAdd(&C->nhs, nch);
+      for (int j = 0; j < nch; ++j) P.hs[t0 + j] = make_int2(v, j);
+    }
   }
   if (!gsync()) return;
 
@@ -433,6 +440,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
               int vv = base + j;
               Seg sg = ops.seg(vv);
               int d = sg.deg();
+              if (d > kChunk) continue;            // hubs: static chunk tasks below
               bool hit = false;
               int scanned = 0;
               for (int b = 0; b < d; b += 32) {
@@ -456,9 +464,36 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
             int dg = found ? ops.degree(v) : 0;
             unsigned fsum = warp_sum((unsigned)dg);
             if (lane == 0) fedges += fsum;
-            bool huge = found && dg > kChunk;
-            if (huge) huge_append(v, dg, o);
-            warp_append(S, cnt, found && !huge, v, o);
+            warp_append(S, cnt, found, v, o);
+          }
+          // unlabelled hubs: one warp per 1024-slot chunk, first finder labels (CAS)
+          const int nhs = ld_cg(&C->nhs);
+          for (int t = gwarp; t < nhs; t += nwarps) {
+            int2 hsk = ld_cg(P.hs + t);
+            int vv = hsk.x;
+            if (ld_cg_hint(P.h + vv, pl) != N) continue;
+            Seg sg = ops.seg(vv);
+            int lo2 = hsk.y * kChunk, hi2 = min(sg.deg(), lo2 + kChunk);
+            bool hit = false;
+            int scanned = 0;
+            for (int b = lo2; b < hi2; b += 32) {
+              int i = b + lane;
+              bool ok = false;
+              if (i < hi2) {
+                int col, cf, slot;
+                ops.out_arc(sg, i, col, cf, slot);
+                ok = cf > 0 && ld_cg_hint(P.h + col, pl) == level;
+              }
+              scanned += 32;
+              if (__ballot_sync(FULL, ok)) { hit = true; break; }
+            }
+            if (lane == 0) {
+              st_bfs_arcs += min(scanned, hi2 - lo2);
+              if (hit && atomicCAS(P.h + vv, N, level + 1) == N) {
+                huge_append(vv, sg.deg(), o);
+                fedges += sg.deg();
+              }
+            }
           }
         }
         {
