@@ -117,6 +117,8 @@ typedef struct wbpr_stats {
   float build_ms, solve_ms, extract_ms, total_ms; /* CUDA-event times on `stream`       */
   int32_t grid_blocks, block_threads;
   int64_t kernel_launches;   /* kernels this call launched (all of them this library's own) */
+  int64_t t_barrier_ns, t_flush_ns, t_round_ns; /* CTA 0 time in grid barriers / queue flushes /
+                                                   round task loops (globaltimer)             */
 } wbpr_stats;
 
 /* Fill *opt with the defaults above. */

@@ -397,6 +397,9 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
     stats->grid_blocks = blocks;
     stats->block_threads = kSolveThreads;
     stats->kernel_launches = launch_count() - launches0;
+    stats->t_barrier_ns = c.stats[ST_COUNT - 3];
+    stats->t_flush_ns = c.stats[ST_COUNT - 2];
+    stats->t_round_ns = c.stats[ST_COUNT - 1];
   }
   if (c.status == DS_NOTCONVERGED) return fail(WBPR_ENOTCONVERGED, "round cap exceeded");
   if (c.abort) return fail(WBPR_ENOTCONVERGED, "device watchdog timeout");

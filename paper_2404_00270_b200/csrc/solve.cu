@@ -247,7 +247,9 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
     o.hq = P.hq[buf]; o.hc = P.hc[buf]; o.hn = &r->hn; o.hc_cnt = &r->hc;
     return o;
   };
+  unsigned long long t_sync = 0, t_flush = 0, t_round = 0;
   auto gsync = [&]() -> bool {
+    const unsigned long long ts0 = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer() : 0;
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned target = gen + 1;
@@ -314,6 +316,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
     ++gen;
     ++ph;
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) t_sync += globaltimer() - ts0;
     return S.abort == 0;
   };
 
@@ -547,6 +550,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
 
     // -------------------------------------------------------------- one push/relabel round
     {
+      const unsigned long long tr0 = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer() : 0;
       const int qn = S.bc.qn, hc = S.bc.hc;
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         C->stats[ST_ROUNDS]++;
@@ -709,9 +713,11 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
         warp_append(S, cnt, lane == 0 && app_u >= 0, app_u, o);
         warp_append(S, cnt, lane == 0 && app_v >= 0, app_v, o);
       }
+      const unsigned long long tf0 = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer() : 0;
       block_flush_all(S, cnt, o);
       unsigned long long t = block_sum_u64(S, work);
       if (threadIdx.x == 0 && t) atomicAdd(&ring(ph)->work, (unsigned)(t < 0x7fffffffull ? t : 0x7fffffffull));
+      if (blockIdx.x == 0 && threadIdx.x == 0) { t_flush += globaltimer() - tf0; t_round += tf0 - tr0; }
       if (!gsync()) return;
       cur ^= 1;
       ++rounds;
@@ -725,6 +731,11 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
   }
 
   // ---------------------------------------------------------------- statistics
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    C->stats[ST_COUNT - 3] = (long long)t_sync;
+    C->stats[ST_COUNT - 2] = (long long)t_flush;
+    C->stats[ST_COUNT - 1] = (long long)t_round;
+  }
   {
     long long v[5] = {st_push, st_relabel, st_arcs, st_bfs_arcs, st_cand};
     int idx[5] = {ST_PUSHES, ST_RELABELS, ST_ARCS, ST_BFS_ARCS, ST_CAND};

@@ -54,7 +54,8 @@ class Stats(ctypes.Structure):
         "self_loops_ignored", "bad_edge_index", "excess_total")] + [
         ("build_ms", ctypes.c_float), ("solve_ms", ctypes.c_float), ("extract_ms", ctypes.c_float),
         ("total_ms", ctypes.c_float), ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
-        ("kernel_launches", ctypes.c_int64)]
+        ("kernel_launches", ctypes.c_int64), ("t_barrier_ns", ctypes.c_int64), ("t_flush_ns", ctypes.c_int64),
+        ("t_round_ns", ctypes.c_int64)]
 
     def as_dict(self):
         return {f[0]: getattr(self, f[0]) for f in self._fields_}
