@@ -306,6 +306,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.gap_mode = opt.gap_mode;
   P.push_mode = opt.push_mode;
   P.bfs_mode = opt.bfs_mode;
+  P.small_mode = opt.small_mode;
   P.gr_gamma = opt.gr_gamma;
   P.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
   int occ = di.occ[opt.layout];
@@ -426,6 +427,7 @@ wbpr_status wbpr_default_options(wbpr_options* opt) {
   opt->gr_gamma = 1.0f;
   opt->l2_persist = 0;
   opt->bfs_mode = 1;
+  opt->small_mode = 1;
   return WBPR_OK;
 }
 

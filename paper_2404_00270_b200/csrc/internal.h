@@ -26,7 +26,8 @@ struct Ring {
   unsigned work;            // relabel work (slots scanned by relabels), saturating
   int kind;                 // PhaseKind of the phase that used this slot
   unsigned fedges;          // BFS: residual slots of the vertices appended to the next frontier
-  int pad[2];
+  int maxdeg;               // largest degree among the appended vertices
+  int pad;
 };
 
 // What the last CTA to arrive at a grid barrier publishes for everyone (one 16-B
@@ -35,10 +36,12 @@ struct __align__(16) Bcast {
   unsigned gen;
   int qn;
   int hc;
-  unsigned flags;   // bit 0: a global relabel is due; bit 1: next BFS level bottom-up
+  unsigned flags;   // bit 0: a global relabel is due; bit 1: next BFS level bottom-up;
+                    // bit 2: run the next phases in the small-frontier CTA mode;
+                    // bit 3: an online gap was found (lift phase before the next round)
 };
 
-enum PhaseKind { PK_NONE = 0, PK_ROUND = 1, PK_GR_RESET = 2, PK_BFS = 3, PK_COMPACT = 4, PK_PREFLOW = 5 };
+enum PhaseKind { PK_NONE = 0, PK_ROUND = 1, PK_GR_RESET = 2, PK_BFS = 3, PK_COMPACT = 4, PK_PREFLOW = 5, PK_GAP = 6 };
 
 // Global-relabel policy state, written only by the last CTA to arrive at a barrier.
 struct GrPolicy {
@@ -65,10 +68,21 @@ struct HugeRec {
 
 enum StatIdx {
   ST_ROUNDS = 0, ST_GRS, ST_BFS_LEVELS, ST_PUSHES, ST_RELABELS, ST_ARCS, ST_BFS_ARCS,
-  ST_CAND, ST_AVQ, ST_GAPLIFT, ST_COUNT = 16
+  ST_CAND, ST_AVQ, ST_GAPLIFT, ST_SMALL_PHASES, ST_SMALL_ENTRIES, ST_COUNT = 16
 };
 
 enum DevStatus { DS_OK = 0, DS_NOTCONVERGED = 1, DS_TIMEOUT = 2, DS_INTERNAL = 3 };
+
+// Hand-off record of the small-frontier mode (CTA 0 runs phases alone; the other
+// CTAs wait on `epoch` and resume the grid loop from this state).
+struct Resume {
+  unsigned epoch;
+  int state;        // next main-loop state
+  int qn, hc;       // counts of the queue the next phase reads
+  int cur, fb, level;
+  int flags;        // Bcast flags for the resumed phase (bit 3: gap lift pending)
+  long long rounds;
+};
 
 // Device control block at the start of the workspace.
 struct Ctrl {
@@ -79,6 +93,8 @@ struct Ctrl {
   int status;
   Ring ring[3];
   GrPolicy pol;
+  Resume res;
+  int small_hn, small_hc;  // huge appends made in the small mode
   long long excess_total;
   long long stats[ST_COUNT];
   // build info
@@ -96,7 +112,8 @@ struct Ctrl {
   int maxlen_out;         // build: longest input row
   int nhs;                // solve: entries of the static huge-chunk list
   int pad0[1];
-  long long gap_level;    // online gap: lowest empty level seen this round (A6)
+  int gap_level;          // online gap: lowest emptied level seen since the last check (A6)
+  int gap_pending;        // the gap level the next lift phase uses
 };
 
 // Byte offsets of every region of a workspace (all 256-B aligned).
@@ -174,6 +191,7 @@ struct SolveParams {
   int gap_mode;
   int push_mode;         // 0: one push to the lowest neighbour (Alg. 2); 1: warp-parallel discharge
   int bfs_mode;          // 0: top-down only; 1: direction-optimizing; 2: bottom-up after level 0
+  int small_mode;        // 1: phases with small queues run in CTA 0 alone (thread per vertex)
   unsigned long long deadline_ns_rel;
 };
 

@@ -141,19 +141,32 @@ WBPR_DEV void st_release_v4(Bcast* p, uint4 v) {
                "r"(v.w) : "memory");
 }
 
+constexpr int kSmallCap = 2048;   // small-frontier mode: shared-memory queue capacity
+constexpr int kSmallMax = 512;    // small-frontier mode: queues up to this size (one pass of 512 threads)
+constexpr int kSmallDeg = 64;     // small-frontier mode: largest degree processed by one thread
+constexpr int kSB = 4;            // small-frontier mode: slots loaded per batch (independent loads)
+constexpr int kGapBins = 256;     // online gap: shared-memory bins for the lowest levels
+
 struct SharedState {
   int buf[kWarps][kBufCap];
   int wsum[kWarps];
+  int wmaxdeg[kWarps];
   unsigned long long wsum64[kWarps];
   int base;
   int abort;
   Bcast bc;           // counts of the phase that just finished
+  int gbin[kGapBins];  // low levels of the height histogram (online gap, A6)
+  // small-frontier mode
+  int sq[2][kSmallCap];
+  int s_n, s_maxdeg, s_huge, s_exit;
+  unsigned long long s_work;
 };
 
 // ------------------------------------------------------------------ warp append buffers
 struct QueueOut {   // next-queue destination
   int* q; int* qn;
   HugeRec* hq; int2* hc; int* hn; int* hc_cnt;
+  int* md;           // largest appended degree (Ring::maxdeg)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() { unsigned r; asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r)); return r; }
@@ -170,10 +183,13 @@ __device__ __forceinline__ void warp_flush(SharedState& S, int& cnt, const Queue
 }
 
 // all lanes call; lanes with pred append val (warp ballot + prefix; AVQ append)
-__device__ __forceinline__ void warp_append(SharedState& S, int& cnt, bool pred, int val, const QueueOut& out) {
+__device__ __forceinline__ void warp_append(SharedState& S, int& cnt, bool pred, int val, const QueueOut& out,
+                                            int dg) {
   unsigned b = __ballot_sync(FULL, pred);
   if (!b) return;
   int w = warp_id();
+  unsigned md = __reduce_max_sync(FULL, pred ? (unsigned)dg : 0u);
+  if (lane_id() == 0 && (int)md > S.wmaxdeg[w]) S.wmaxdeg[w] = (int)md;
   if (pred) S.buf[w][cnt + __popc(b & lanemask_lt())] = val;
   cnt += __popc(b);
   if (cnt >= kBufFlush) warp_flush(S, cnt, out);
@@ -196,9 +212,13 @@ __device__ __forceinline__ void block_flush_all(SharedState& S, int& cnt, const 
   if (lane == 0) S.wsum[w] = cnt;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int i = 0; i < kWarps; ++i) { int c = S.wsum[i]; S.wsum[i] = tot; tot += c; }
+    int tot = 0, md = 0;
+    for (int i = 0; i < kWarps; ++i) {
+      int c = S.wsum[i]; S.wsum[i] = tot; tot += c;
+      md = max(md, S.wmaxdeg[i]); S.wmaxdeg[i] = 0;
+    }
     S.base = tot ? atomicAdd(out.qn, tot) : 0;
+    if (md && out.md) atomicMax(out.md, md);
   }
   __syncthreads();
   int base = S.base + S.wsum[w];
@@ -218,7 +238,7 @@ __device__ __forceinline__ unsigned long long block_sum_u64(SharedState& S, unsi
 }
 
 template <class Ops>
-__global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, const Ops ops_in) {
+__global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P, const Ops ops_in) {
   __shared__ SharedState S;
   Ops ops = ops_in;
   ops.init();
@@ -245,6 +265,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
     Ring* r = ring(ph);
     o.q = P.q[buf]; o.qn = &r->qn;
     o.hq = P.hq[buf]; o.hc = P.hc[buf]; o.hn = &r->hn; o.hc_cnt = &r->hc;
+    o.md = &r->maxdeg;
     return o;
   };
   unsigned long long t_sync = 0, t_flush = 0, t_round = 0;
@@ -271,6 +292,10 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
           bool due = qn + hc == 0 || G.work_since_gr >= gr_threshold ||
                      (P.gr_gamma > 0.f && (double)(now - G.t_after_gr) >= (double)P.gr_gamma * (double)G.gr_time);
           if (due) { flags = 1; G.t_gr_start = now; }
+          else if (P.gap_mode) {
+            const int gl = ld_cg(&C->gap_level);
+            if (gl < N) { flags |= 8; C->gap_pending = gl; C->gap_level = N; }
+          }
         } else if (kind == PK_PREFLOW) {
           G.t_gr_start = now;
         } else if (kind == PK_GR_RESET || kind == PK_BFS) {
@@ -287,16 +312,27 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
           if (P.bfs_mode == 2) G.bfs_bottom_up = 1;
           if (G.bfs_bottom_up) flags |= 2;
         } else if (kind == PK_COMPACT) {
+          C->gap_level = N;
           G.gr_time = now - G.t_gr_start;
           G.t_after_gr = now;
           G.work_since_gr = 0;
+        }
+        // small-frontier mode for the next phase: a round or a top-down BFS level whose
+        // queue fits one CTA (no hub tasks, every queued vertex <= kSmallDeg slots)
+        {
+          int next = 0;
+          if (kind == PK_ROUND) next = (flags & 1) ? 0 : 1;
+          else if (kind == PK_GR_RESET || kind == PK_BFS) next = (qn + hc > 0 && !(flags & 2)) ? 2 : 0;
+          else if (kind == PK_COMPACT) next = (qn + hc > 0) ? 1 : 0;
+          const int md = ld_cg(&r->maxdeg);
+          if (P.small_mode && next && hc == 0 && qn > 0 && qn <= kSmallMax && md <= kSmallDeg) flags |= 4;
         }
         b.x = target;
         b.y = (unsigned)qn;
         b.z = (unsigned)hc;
         b.w = flags;
         Ring* z = ring(ph + 1);
-        z->qn = 0; z->hn = 0; z->hc = 0; z->work = 0; z->kind = 0; z->fedges = 0;
+        z->qn = 0; z->hn = 0; z->hc = 0; z->work = 0; z->kind = 0; z->fedges = 0; z->maxdeg = 0;
         st_release_v4(&C->bc, b);
       } else {
         unsigned ns = 0;
@@ -321,6 +357,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
   };
 
   // ---------------------------------------------------------------- init
+  if (blockIdx.x == 0 && threadIdx.x == 0) C->gap_level = N;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
     st_cg(P.e + v, 0ll);
     P.deact[v] = 0;
@@ -357,16 +394,262 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
   }
   if (!gsync()) return;
 
-  long long rounds = 0;
-  int cur = 0;          // queue buffer holding the current AVQ
-  bool need_gr = true;
 
-  while (true) {
-    if (need_gr) {
+  // ---------------------------------------------------------------- small-frontier mode helpers
+  // CTA 0 alone, one THREAD per queued vertex (<= kSmallDeg slots, 8-slot batches of
+  // independent loads), queues in shared memory, __syncthreads instead of grid barriers.
+  // online gap (A6): height histogram updated at every relabel; a level that empties
+  // is recorded and lifted at the next round boundary (a heuristic under relaxed labels,
+  // corrected by the next exact GR; never used for termination or Excess_total)
+  auto gap_relabel = [&](int old, int nh) {
+    if (!P.gap_mode) return;
+    if (old < N) {
+      int prev = atomicSub(P.hist + old, 1);
+      if (prev == 1) atomicMin(&C->gap_level, old);
+    }
+    if (nh < N) atomicAdd(P.hist + nh, 1);
+  };
+  int sa = 0, sdst = 0;   // shared-memory queue being read; global queue buffer being written
+  auto small_append = [&](int v, int dg) {
+    if (dg > kChunk) {
+      QueueOut ho;
+      ho.q = nullptr; ho.qn = nullptr; ho.md = nullptr;
+      ho.hq = P.hq[sdst]; ho.hc = P.hc[sdst]; ho.hn = &C->small_hn; ho.hc_cnt = &C->small_hc;
+      huge_append(v, dg, ho);
+      S.s_huge = 1;
+      return;
+    }
+    int pos = atomicAdd(&S.s_n, 1);
+    st_cg(P.q[sdst] + pos, v);                 // complete copy in global memory (grid resume)
+    if (pos < kSmallCap) S.sq[sa ^ 1][pos] = v;
+    atomicMax(&S.s_maxdeg, dg);
+  };
+  auto small_round_vertex = [&](int u) {
+    Seg sg = ops.seg(u);
+    const int d = sg.deg();
+    const int hu = ld_cg(P.h + u);
+    const long long eu = ld_cg(P.e + u);
+    if (hu >= N) return;   // lifted by the gap heuristic: inactive until the next GR
+    unsigned long long best = ~0ull;
+    int bcf = 0, bcol = 0;
+    long long budget = eu, pushed = 0;
+    for (int b0 = 0; b0 < d; b0 += kSB) {
+      int col[kSB], cf[kSB], slot[kSB], hv[kSB];
+#pragma unroll
+      for (int j = 0; j < kSB; ++j) {
+        cf[j] = 0; col[j] = 0; slot[j] = 0;
+        if (b0 + j < d) ops.out_arc(sg, b0 + j, col[j], cf[j], slot[j]);
+      }
+      int dgc[kSB];
+#pragma unroll
+      for (int j = 0; j < kSB; ++j) {
+        hv[j] = cf[j] > 0 ? ld_cg_hint(P.h + col[j], pl) : INT_MAX;
+        dgc[j] = (P.push_mode != 0 && cf[j] > 0) ? ops.degree(col[j]) : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < kSB; ++j) {
+        if (cf[j] > 0) {
+          unsigned long long cand = ((unsigned long long)(unsigned)hv[j] << 32) | (unsigned)slot[j];
+          if (cand < best) { best = cand; bcf = cf[j]; bcol = col[j]; }
+        }
+      }
+      if (P.push_mode != 0) {
+#pragma unroll
+        for (int j = 0; j < kSB; ++j) {
+          if (cf[j] > 0 && hv[j] < hu && budget > 0) {
+            int dd = (int)(budget < (long long)cf[j] ? budget : (long long)cf[j]);
+            int dgv = dgc[j];
+            ops.push(slot[j], dd);
+            long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col[j]), (unsigned long long)dd);
+            if (old_v == 0 && __ldg(P.term + col[j]) == 0) small_append(col[j], dgv);
+            budget -= dd;
+            pushed += dd;
+            ++st_push;
+          }
+        }
+        if (budget <= 0) break;
+      }
+    }
+    st_arcs += d;
+    const unsigned hmin = (unsigned)(best >> 32);
+    if (P.push_mode == 0 && best != ~0ull && (int)hmin < hu && bcf > 0) {
+      int dd = (int)(eu < (long long)bcf ? eu : (long long)bcf);
+      int dgv = ops.degree(bcol);
+      ops.push((int)(best & 0xffffffffu), dd);
+      long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-(long long)dd));
+      long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + bcol), (unsigned long long)dd);
+      if (old_u - dd > 0) small_append(u, d);
+      if (old_v == 0 && __ldg(P.term + bcol) == 0) small_append(bcol, dgv);
+      ++st_push;
+    } else if (P.push_mode != 0 && pushed > 0) {
+      long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-pushed));
+      if (old_u - pushed > 0) small_append(u, d);
+    } else {
+      int nh = (best == ~0ull || (int)hmin >= N - 1) ? N : (int)hmin + 1;
+      st_cg(P.h + u, nh);
+      gap_relabel(hu, nh);
+      if (nh < N) small_append(u, d);
+      atomicAdd(&S.s_work, (unsigned long long)d + 1);
+      ++st_relabel;
+    }
+  };
+  auto small_bfs_vertex = [&](int wv, int lvl) {
+    Seg sg = ops.seg(wv);
+    const int d = sg.deg();
+    for (int b0 = 0; b0 < d; b0 += kSB) {
+      int u[kSB], cf[kSB], hu8[kSB];
+#pragma unroll
+      for (int j = 0; j < kSB; ++j) {
+        cf[j] = 0; u[j] = 0;
+        if (b0 + j < d) ops.in_arc(sg, b0 + j, u[j], cf[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kSB; ++j) hu8[j] = cf[j] > 0 ? ld_cg_hint(P.h + u[j], pl) : -1;
+#pragma unroll
+      for (int j = 0; j < kSB; ++j)
+        if (cf[j] > 0 && hu8[j] == N && atomicCAS(P.h + u[j], N, lvl + 1) == N) small_append(u[j], ops.degree(u[j]));
+    }
+    st_bfs_arcs += d;
+  };
+
+  enum { S_GR = 0, S_BFS = 1, S_COMPACT = 2, S_ROUND = 3, S_DONE = 4 };
+  long long rounds = 0;
+  int cur = 0, fb = 0, level = 0;
+  int state = S_GR;
+  unsigned small_epoch = 0;
+
+  while (state != S_DONE) {
+    if (state == S_ROUND && (S.bc.flags & 8)) {
+      // ------------------------------------------------------------ gap lift (A6)
+      const int sqn = S.bc.qn, shc = S.bc.hc;
+      const int gl = ld_cg(&C->gap_pending);
+      unsigned long long lifted = 0;
+      for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
+        int hv = ld_cg(P.h + v);
+        if (hv > gl && hv < N) {
+          st_cg(P.h + v, N);
+          atomicSub(P.hist + hv, 1);
+          ++lifted;
+        }
+      }
+      unsigned long long t = block_sum_u64(S, lifted);
+      if (threadIdx.x == 0 && t) atomicAdd((unsigned long long*)&C->stats[ST_GAPLIFT], t);
+      if (blockIdx.x == 0 && threadIdx.x == 0) ring(ph)->kind = PK_GAP;
+      if (!gsync()) return;
+      if (threadIdx.x == 0) { S.bc.qn = sqn; S.bc.hc = shc; S.bc.flags = 0; }
+      __syncthreads();
+      continue;
+    }
+    if (S.bc.flags & 4) {
+      // ------------------------------------------------------------ small-frontier mode
+      if (blockIdx.x == 0) {
+        int qa = S.bc.qn;
+        const int* gsrc = (state == S_BFS) ? P.q[fb] : P.q[cur];
+        for (int i = threadIdx.x; i < qa; i += blockDim.x) S.sq[0][i] = ld_cg(gsrc + i);
+        // thread 0 keeps the GR-policy state and counters in registers while CTA 0 runs alone
+        unsigned long long g_work = 0, g_after = 0, g_grtime = 0;
+        long long c_rounds = 0, c_avq = 0, c_levels = 0, c_phases = 0;
+        if (threadIdx.x == 0) {
+          C->small_hn = 0; C->small_hc = 0; C->stats[ST_SMALL_ENTRIES]++;
+          g_work = C->pol.work_since_gr; g_after = C->pol.t_after_gr; g_grtime = C->pol.gr_time;
+        }
+        sa = 0;
+        int code = 0, nn = 0;
+        __syncthreads();
+        while (true) {
+          if (threadIdx.x == 0) { S.s_n = 0; S.s_maxdeg = 0; S.s_huge = 0; S.s_work = 0; S.s_exit = 0; }
+          sdst = (state == S_BFS) ? (fb ^ 1) : (cur ^ 1);
+          __syncthreads();
+          if (state == S_BFS) {
+            for (int i = threadIdx.x; i < qa; i += blockDim.x) small_bfs_vertex(S.sq[sa][i], level);
+          } else {
+            if (threadIdx.x == 0) { ++c_rounds; c_avq += qa; }
+            for (int i = threadIdx.x; i < qa; i += blockDim.x) small_round_vertex(S.sq[sa][i]);
+          }
+          __syncthreads();
+          nn = S.s_n;
+          if (state == S_BFS) { fb ^= 1; ++level; } else { cur ^= 1; ++rounds; }
+          if (threadIdx.x == 0) {
+            ++c_phases;
+            int ex = 0;
+            const unsigned long long now = globaltimer();
+            const bool spill = nn > kSmallMax || S.s_maxdeg > kSmallDeg || S.s_huge;
+            if (state == S_BFS) {
+              ++c_levels;
+              if (nn == 0 && !S.s_huge) ex = 2;
+              else if (spill) ex = 1;
+            } else {
+              g_work += S.s_work;
+              bool due = (nn == 0 && !S.s_huge) || g_work >= gr_threshold ||
+                         (P.gr_gamma > 0.f && (double)(now - g_after) >= (double)P.gr_gamma * (double)g_grtime);
+              if (due) { C->pol.t_gr_start = now; ex = 3; }
+              else if (rounds >= P.max_rounds) { C->status = DS_NOTCONVERGED; ex = 4; }
+              else if (P.gap_mode && ld_cg(&C->gap_level) < N) {
+                C->gap_pending = C->gap_level; C->gap_level = N; ex = 6;
+              }
+              else if (spill) ex = 1;
+            }
+            if (!ex && (ld_volatile(&C->abort) || now > deadline)) { atomicExch(&C->abort, 1); ex = 5; }
+            S.s_exit = ex;
+          }
+          __syncthreads();
+          code = S.s_exit;
+          if (code) break;
+          qa = nn;
+          sa ^= 1;
+        }
+        if (code == 2) state = S_COMPACT;
+        else if (code == 3) state = S_GR;
+        else if (code == 4 || code == 5) state = S_DONE;
+        if (threadIdx.x == 0) {
+          C->pol.work_since_gr = g_work;
+          C->stats[ST_ROUNDS] += c_rounds; C->stats[ST_AVQ] += c_avq;
+          C->stats[ST_BFS_LEVELS] += c_levels; C->stats[ST_SMALL_PHASES] += c_phases;
+          Resume& R = C->res;
+          R.state = state; R.qn = nn; R.hc = C->small_hc; R.cur = cur; R.fb = fb; R.level = level;
+          R.rounds = rounds;
+          R.flags = code == 6 ? 8 : 0;
+          __threadfence();
+          atomicAdd(&R.epoch, 1u);
+          S.bc.qn = nn; S.bc.hc = C->small_hc; S.bc.flags = code == 6 ? 8 : 0;
+          S.abort = code == 5;
+        }
+        ++small_epoch;
+        __syncthreads();
+        if (S.abort) return;
+      } else {
+        if (threadIdx.x == 0) {
+          const unsigned target = small_epoch + 1;
+          int ab = 0;
+          unsigned ns = 32;
+          while (ld_acquire(&C->res.epoch) != target) {
+            if (ld_volatile(&C->abort)) { ab = 1; break; }
+            if (globaltimer() > deadline) { atomicExch(&C->abort, 1); ab = 1; break; }
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+          }
+          Resume& R = C->res;
+          S.bc.qn = ld_cg(&R.qn); S.bc.hc = ld_cg(&R.hc); S.bc.flags = (unsigned)ld_cg(&R.flags);
+          S.s_n = ld_cg(&R.state); S.s_maxdeg = ld_cg(&R.cur); S.s_huge = ld_cg(&R.fb); S.s_exit = ld_cg(&R.level);
+          S.s_work = (unsigned long long)ld_cg(&R.rounds);
+          S.abort = ab;
+        }
+        __syncthreads();
+        if (S.abort) return;
+        state = S.s_n; cur = S.s_maxdeg; fb = S.s_huge; level = S.s_exit; rounds = (long long)S.s_work;
+        ++small_epoch;
+        __syncthreads();
+      }
+      continue;
+    }
+
+    if (state == S_GR) {
       // ------------------------------------------------------------ global relabel
       // reset labels: sinks 0, everything else |V| (= unreached); frontier <- sinks
-      for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x)
+      for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
         st_cg(P.h + v, (__ldg(P.term + v) & kSink) ? 0 : ((__ldg(P.term + v) & kSource) ? N + 1 : N));
+        if (P.gap_mode) st_cg(P.hist + v, 0);
+      }
       if (blockIdx.x == 0) {
         QueueOut o = out_for(0);
         for (int base = w * 32; base < P.k; base += kWarps * 32) {
@@ -375,7 +658,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
           int dg = i < P.k ? ops.degree(t) : 0;
           bool huge = i < P.k && dg > kChunk;
           if (huge) huge_append(t, dg, o);
-          warp_append(S, cnt, i < P.k && !huge, t, o);
+          warp_append(S, cnt, i < P.k && !huge, t, o, dg);
           unsigned fsum = warp_sum((unsigned)dg);
           if (lane == 0 && fsum) atomicAdd(&ring(ph)->fedges, fsum);
         }
@@ -383,10 +666,16 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
         if (threadIdx.x == 0) { C->stats[ST_GRS]++; ring(ph)->kind = PK_GR_RESET; }
       }
       if (!gsync()) return;
-      int fb = 0, level = 0;
-      while (true) {
-        int qn = S.bc.qn, hc = S.bc.hc;
-        if (qn + hc == 0) break;
+      state = S_BFS;
+      fb = 0;
+      level = 0;
+      continue;
+    }
+
+    if (state == S_BFS) {
+      int qn = S.bc.qn, hc = S.bc.hc;
+      if (qn + hc == 0) { state = S_COMPACT; continue; }
+      {
         QueueOut o = out_for(fb ^ 1);
         unsigned fedges = 0;   // lane 0: slots of the vertices this warp appended
         if (!(S.bc.flags & 2)) {
@@ -426,7 +715,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
               if (lane == 0) fedges += fsum;
               bool huge = found && dg > kChunk;
               if (huge) huge_append(u, dg, o);
-              warp_append(S, cnt, found && !huge, u, o);
+              warp_append(S, cnt, found && !huge, u, o, dg);
             }
           }
         } else {
@@ -467,7 +756,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
             int dg = found ? ops.degree(v) : 0;
             unsigned fsum = warp_sum((unsigned)dg);
             if (lane == 0) fedges += fsum;
-            warp_append(S, cnt, found, v, o);
+            warp_append(S, cnt, found, v, o, dg);
           }
           // unlabelled hubs: one warp per 1024-slot chunk, first finder labels (CAS)
           const int nhs = ld_cg(&C->nhs);
@@ -505,19 +794,32 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
         }
         block_flush_all(S, cnt, o);
         if (blockIdx.x == 0 && threadIdx.x == 0) { C->stats[ST_BFS_LEVELS]++; ring(ph)->kind = PK_BFS; }
-        if (!gsync()) return;
-        fb ^= 1;
-        ++level;
       }
+      if (!gsync()) return;
+      fb ^= 1;
+      ++level;
+      continue;
+    }
+
+    if (state == S_COMPACT) {
       // ------------------------------------------------------------ full compaction (Alg. 2 l.1-4)
       // + Excess_total bookkeeping for vertices the GR found unable to reach a sink
       {
         QueueOut o = out_for(0);
         unsigned long long dropped = 0;
+        if (P.gap_mode) {
+          for (int i = threadIdx.x; i < kGapBins; i += blockDim.x) S.gbin[i] = 0;
+          __syncthreads();
+        }
         for (int base = blockIdx.x * blockDim.x + w * 32; base < N; base += nb * blockDim.x) {
           int v = base + lane;
           bool act = false, huge = false;
           int dg = 0;
+          if (P.gap_mode && v < N) {
+            int hv0 = ld_cg(P.h + v);
+            if (hv0 < kGapBins) atomicAdd(&S.gbin[hv0], 1);
+            else if (hv0 < N) atomicAdd(P.hist + hv0, 1);
+          }
           if (v < N) {
             long long ev = ld_cg(P.e + v);
             if (ev > 0 && __ldg(P.term + v) == 0) {
@@ -534,18 +836,21 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
           }
           if (lane == 0) st_cand += min(32, N - base);
           if (huge) huge_append(v, dg, o);
-          warp_append(S, cnt, act && !huge, v, o);
+          warp_append(S, cnt, act && !huge, v, o, dg);
         }
         block_flush_all(S, cnt, o);
         unsigned long long t = block_sum_u64(S, dropped);
         if (threadIdx.x == 0 && t) atomicAdd((unsigned long long*)&C->excess_total, (unsigned long long)(-(long long)t));
         if (blockIdx.x == 0 && threadIdx.x == 0) ring(ph)->kind = PK_COMPACT;
+        if (P.gap_mode)
+          for (int i = threadIdx.x; i < kGapBins && i < N; i += blockDim.x)
+            if (S.gbin[i]) atomicAdd(P.hist + i, S.gbin[i]);
       }
       if (!gsync()) return;
       cur = 0;
-      need_gr = false;
       // termination: right after an exact GR, no active vertex <=> e(s)+e(t) >= Excess_total
-      if (S.bc.qn + S.bc.hc == 0) break;
+      state = (S.bc.qn + S.bc.hc == 0) ? S_DONE : S_ROUND;
+      continue;
     }
 
     // -------------------------------------------------------------- one push/relabel round
@@ -576,6 +881,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
         Seg sg = ops.seg(u);
         const int hu = ld_cg(P.h + u);
         const long long eu = ld_cg(P.e + u);
+        if (hu >= N) continue;   // lifted by the gap heuristic: inactive until the next GR
         if (hidx < 0) { lo = 0; hi = sg.deg(); } else { hi = min(sg.deg(), lo + kChunk); }
         if (lane == 0) st_arcs += hi - lo;
 
@@ -647,7 +953,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
             int dgv = app ? ops.degree(col) : 0;
             bool hugev = app && dgv > kChunk;
             if (hugev) huge_append(col, dgv, o);
-            warp_append(S, cnt, app && !hugev, col, o);
+            warp_append(S, cnt, app && !hugev, col, o, dgv);
             if (hidx < 0 && budget <= 0) break;
           }
         }
@@ -703,6 +1009,7 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
             // relabel: h(u) <- h' + 1 (Alg. 1 line 21); >= |V| deactivates
             int nh = (hmin == kInf || (int)hmin >= N - 1) ? N : (int)hmin + 1;
             st_cg(P.h + u, nh);
+            gap_relabel(hu, nh);
             if (nh < N) { app_u = u; dgu = sg.deg(); }
             work += (unsigned long long)sg.deg() + 1;
             ++st_relabel;
@@ -710,8 +1017,8 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
           if (app_u >= 0 && dgu > kChunk) { huge_append(app_u, dgu, o); app_u = -1; }
           if (app_v >= 0 && dgv > kChunk) { huge_append(app_v, dgv, o); app_v = -1; }
         }
-        warp_append(S, cnt, lane == 0 && app_u >= 0, app_u, o);
-        warp_append(S, cnt, lane == 0 && app_v >= 0, app_v, o);
+        warp_append(S, cnt, lane == 0 && app_u >= 0, app_u, o, dgu);
+        warp_append(S, cnt, lane == 0 && app_v >= 0, app_v, o, dgv);
       }
       const unsigned long long tf0 = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer() : 0;
       block_flush_all(S, cnt, o);
@@ -723,10 +1030,11 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve(const SolveParams P, co
       ++rounds;
       if (rounds >= P.max_rounds) {
         if (blockIdx.x == 0 && threadIdx.x == 0) { C->status = DS_NOTCONVERGED; }
-        break;
+        state = S_DONE;
+        continue;
       }
       // early break / periodic GR, decided by the barrier's last arriver
-      if (S.bc.flags & 1) need_gr = true;
+      if (S.bc.flags & 1) state = S_GR;
     }
   }
 

@@ -163,12 +163,14 @@ def test_gr_frequency_and_grid_size_invariance(layout):
 @pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("push_mode", [0, 1])
 @pytest.mark.parametrize("bfs_mode", [0, 1, 2])
-def test_modes(layout, push_mode, bfs_mode):
+@pytest.mark.parametrize("small_mode", [0, 1])
+@pytest.mark.parametrize("gap_mode", [0, 1])
+def test_modes(layout, push_mode, bfs_mode, small_mode, gap_mode):
     # the paper's single push (Alg. 2) and the discharge deviation; top-down, direction-
     # optimizing and bottom-up BFS: all must reach the same unique F / cut / S*
     for g in (synth.rmat(12, 16, 7, "hub20"), synth.grid(40, 30, True, 2),
               synth.tiny_random(9, 30, 5, 3), synth.random_graph(800, 6000, 5, 0, 799)):
-        assert_parity(g, layout, push_mode=push_mode, bfs_mode=bfs_mode)
+        assert_parity(g, layout, push_mode=push_mode, bfs_mode=bfs_mode, small_mode=small_mode, gap_mode=gap_mode)
 
 
 # ------------------------------------------------------------------ host-buffer path (e2e)
