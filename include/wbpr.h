@@ -95,8 +95,8 @@ typedef struct wbpr_options {
   int32_t bfs_mode;      /* global-relabel BFS: 0 top-down only; 1 (default) direction-
                             optimizing (bottom-up levels while the frontier is large);
                             2 bottom-up from the first level (testing)                      */
-  int32_t small_mode;    /* 1 (default): phases whose queue fits one CTA (<= 2048 vertices of
-                            <= 64 slots) run in CTA 0 alone, one thread per vertex, with
+  int32_t small_mode;    /* 1 (default): phases whose queue fits one CTA (<= 512 vertices of
+                            <= 8 slots) run in CTA 0 alone, one thread per vertex, with
                             block barriers instead of grid barriers; 0: off                 */
   int32_t reserved[1];
 } wbpr_options;

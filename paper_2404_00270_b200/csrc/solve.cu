@@ -143,7 +143,7 @@ WBPR_DEV void st_release_v4(Bcast* p, uint4 v) {
 
 constexpr int kSmallCap = 2048;   // small-frontier mode: shared-memory queue capacity
 constexpr int kSmallMax = 512;    // small-frontier mode: queues up to this size (one pass of 512 threads)
-constexpr int kSmallDeg = 64;     // small-frontier mode: largest degree processed by one thread
+constexpr int kSmallDeg = 8;      // small-frontier mode: largest degree processed by one thread
 constexpr int kSB = 4;            // small-frontier mode: slots loaded per batch (independent loads)
 constexpr int kGapBins = 256;     // online gap: shared-memory bins for the lowest levels
 
