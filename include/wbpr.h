@@ -98,7 +98,10 @@ typedef struct wbpr_options {
   int32_t small_mode;    /* 1 (default): phases whose queue fits one CTA (<= 512 vertices of
                             <= 8 slots) run in CTA 0 alone, one thread per vertex, with
                             block barriers instead of grid barriers; 0: off                 */
-  int32_t reserved[1];
+  int32_t schedule;      /* 0 (default): vertex-centric - active-vertex queue, one warp per
+                            active vertex (Alg. 2, the paper's method); 1: thread-centric -
+                            every sweep one thread per vertex tests activity and scans the
+                            residual arcs serially (Alg. 1 Step 1, the paper's baseline)     */
 } wbpr_options;
 
 typedef struct wbpr_stats {

@@ -209,6 +209,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   if (s) return s;
   wbpr_options opt = resolve(opt_in);
   if (opt.layout != WBPR_LAYOUT_BCSR && opt.layout != WBPR_LAYOUT_RCSR) return fail(WBPR_EINVAL, "unknown layout");
+  if (opt.schedule != 0 && opt.schedule != 1) return fail(WBPR_EINVAL, "unknown schedule");
   const int64_t n = g->n, m = g->m;
   if (k < 1 || k > kMaxInst) return fail(WBPR_EINVAL, "instance count out of range");
   if (vbase_h[0] != 0 || vbase_h[k] != n) return fail(WBPR_EINVAL, "vbase must start at 0 and end at n");
@@ -307,6 +308,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.push_mode = opt.push_mode;
   P.bfs_mode = opt.bfs_mode;
   P.small_mode = opt.small_mode;
+  P.schedule = opt.schedule;
   P.gr_gamma = opt.gr_gamma;
   P.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
   int occ = di.occ[opt.layout];

@@ -192,6 +192,7 @@ struct SolveParams {
   int push_mode;         // 0: one push to the lowest neighbour (Alg. 2); 1: warp-parallel discharge
   int bfs_mode;          // 0: top-down only; 1: direction-optimizing; 2: bottom-up after level 0
   int small_mode;        // 1: phases with small queues run in CTA 0 alone (thread per vertex)
+  int schedule;          // 0: vertex-centric (AVQ + warp per vertex, Alg. 2); 1: thread-centric sweeps (Alg. 1)
   unsigned long long deadline_ns_rel;
 };
 

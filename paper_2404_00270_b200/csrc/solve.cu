@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           else if (kind == PK_GR_RESET || kind == PK_BFS) next = (qn + hc > 0 && !(flags & 2)) ? 2 : 0;
           else if (kind == PK_COMPACT) next = (qn + hc > 0) ? 1 : 0;
           const int md = ld_cg(&r->maxdeg);
-          if (P.small_mode && next && hc == 0 && qn > 0 && qn <= kSmallMax && md <= kSmallDeg) flags |= 4;
+          if (P.small_mode && P.schedule == 0 && next && hc == 0 && qn > 0 && qn <= kSmallMax && md <= kSmallDeg) flags |= 4;
         }
         b.x = target;
         b.y = (unsigned)qn;
@@ -424,7 +424,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     if (pos < kSmallCap) S.sq[sa ^ 1][pos] = v;
     atomicMax(&S.s_maxdeg, dg);
   };
-  auto small_round_vertex = [&](int u) {
+  // tc = true: thread-centric sweep (Alg. 1 Step 1, NEXT #1) - no queue appends
+  unsigned long long tc_work = 0;
+  auto small_round_vertex = [&](int u, bool tc) {
     Seg sg = ops.seg(u);
     const int d = sg.deg();
     const int hu = ld_cg(P.h + u);
@@ -461,7 +463,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
             int dgv = dgc[j];
             ops.push(slot[j], dd);
             long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col[j]), (unsigned long long)dd);
-            if (old_v == 0 && __ldg(P.term + col[j]) == 0) small_append(col[j], dgv);
+            if (!tc && old_v == 0 && __ldg(P.term + col[j]) == 0) small_append(col[j], dgv);
             budget -= dd;
             pushed += dd;
             ++st_push;
@@ -478,18 +480,19 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       ops.push((int)(best & 0xffffffffu), dd);
       long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-(long long)dd));
       long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + bcol), (unsigned long long)dd);
-      if (old_u - dd > 0) small_append(u, d);
-      if (old_v == 0 && __ldg(P.term + bcol) == 0) small_append(bcol, dgv);
+      if (!tc && old_u - dd > 0) small_append(u, d);
+      if (!tc && old_v == 0 && __ldg(P.term + bcol) == 0) small_append(bcol, dgv);
       ++st_push;
     } else if (P.push_mode != 0 && pushed > 0) {
       long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-pushed));
-      if (old_u - pushed > 0) small_append(u, d);
+      if (!tc && old_u - pushed > 0) small_append(u, d);
     } else {
       int nh = (best == ~0ull || (int)hmin >= N - 1) ? N : (int)hmin + 1;
       st_cg(P.h + u, nh);
       gap_relabel(hu, nh);
-      if (nh < N) small_append(u, d);
-      atomicAdd(&S.s_work, (unsigned long long)d + 1);
+      if (!tc && nh < N) small_append(u, d);
+      if (tc) tc_work += (unsigned long long)d + 1;
+      else atomicAdd(&S.s_work, (unsigned long long)d + 1);
       ++st_relabel;
     }
   };
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
   unsigned small_epoch = 0;
 
   while (state != S_DONE) {
-    if (state == S_ROUND && (S.bc.flags & 8)) {
+    if (state == S_ROUND && (S.bc.flags & 8)) {   // (TC sweeps skip lifted vertices by h >= n)
       // ------------------------------------------------------------ gap lift (A6)
       const int sqn = S.bc.qn, shc = S.bc.hc;
       const int gl = ld_cg(&C->gap_pending);
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
             for (int i = threadIdx.x; i < qa; i += blockDim.x) small_bfs_vertex(S.sq[sa][i], level);
           } else {
             if (threadIdx.x == 0) { ++c_rounds; c_avq += qa; }
-            for (int i = threadIdx.x; i < qa; i += blockDim.x) small_round_vertex(S.sq[sa][i]);
+            for (int i = threadIdx.x; i < qa; i += blockDim.x) small_round_vertex(S.sq[sa][i], false);
           }
           __syncthreads();
           nn = S.s_n;
@@ -850,6 +853,37 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       cur = 0;
       // termination: right after an exact GR, no active vertex <=> e(s)+e(t) >= Excess_total
       state = (S.bc.qn + S.bc.hc == 0) ? S_DONE : S_ROUND;
+      continue;
+    }
+
+    if (P.schedule == 1) {
+      // ------------------------------------------------------------ thread-centric sweep
+      // Alg. 1 Step 1: every thread tests its vertices for activity and scans
+      // their residual arcs serially (NEXT #1: the paper's comparison baseline)
+      if (blockIdx.x == 0 && threadIdx.x == 0) { C->stats[ST_ROUNDS]++; ring(ph)->kind = PK_ROUND; }
+      unsigned long long active = 0;
+      tc_work = 0;
+      for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
+        if (ld_cg(P.e + v) > 0 && __ldg(P.term + v) == 0 && ld_cg(P.h + v) < N) {
+          ++active;
+          small_round_vertex(v, true);
+        }
+      }
+      if (lane == 0) st_cand += 0;
+      unsigned long long ta = block_sum_u64(S, active);
+      unsigned long long tw = block_sum_u64(S, tc_work);
+      if (threadIdx.x == 0) {
+        if (ta) atomicAdd(&ring(ph)->qn, (int)ta);   // "queue" size = active vertices found
+        if (tw) atomicAdd(&ring(ph)->work, (unsigned)(tw < 0x7fffffffull ? tw : 0x7fffffffull));
+      }
+      if (!gsync()) return;
+      ++rounds;
+      if (rounds >= P.max_rounds) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) { C->status = DS_NOTCONVERGED; }
+        state = S_DONE;
+        continue;
+      }
+      if (S.bc.flags & 1) state = S_GR;
       continue;
     }
 

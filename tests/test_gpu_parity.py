@@ -256,3 +256,13 @@ def test_errors():
     rc = L.wbpr_maxflow_solve(ctypes.byref(c), 0, 99, ctypes.byref(W.options()), small.ptr, 1024, None, None,
                               ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     assert rc == -3  # WBPR_ENOMEM
+
+
+# ------------------------------------------------------------------ thread-centric schedule (NEXT #1)
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("push_mode", [0, 1])
+def test_thread_centric(layout, push_mode):
+    # Alg. 1 Step 1: one thread per vertex per sweep; same unique F / cut / S* as the VC path
+    for g in (synth.rmat(12, 16, 7, "paper"), synth.rmat(11, 16, 3, "hub20"), synth.grid(30, 20, True, 1),
+              synth.random_graph(600, 5000, 2, 0, 599), synth.tiny_random(10, 40, 6, 9)):
+        assert_parity(g, layout, schedule="tc", push_mode=push_mode)

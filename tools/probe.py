@@ -36,6 +36,7 @@ ap.add_argument("--persist", type=int, default=0)
 ap.add_argument("--bfs", type=int, default=1)
 ap.add_argument("--small", type=int, default=1)
 ap.add_argument("--gap", type=int, default=0)
+ap.add_argument("--schedule", default="vc")
 ap.add_argument("--oracle", action="store_true")
 a = ap.parse_args()
 for name in a.cfgs:
@@ -46,7 +47,7 @@ for name in a.cfgs:
         gen = time.time() - t0
         for rep in range(a.reps):
             size, match, st = W.bipartite_match(1 << 20, 1 << 20, lt, rt, layout=a.layout, gr_beta=a.beta,
-                                                timeout_ms=100000, grid_blocks=a.blocks, push_mode=a.mode, gr_gamma=a.gamma, l2_persist=a.persist, bfs_mode=a.bfs, small_mode=a.small, gap_mode=a.gap)
+                                                timeout_ms=100000, grid_blocks=a.blocks, push_mode=a.mode, gr_gamma=a.gamma, l2_persist=a.persist, bfs_mode=a.bfs, small_mode=a.small, gap_mode=a.gap, schedule=a.schedule)
             print(json.dumps(dict(cfg=name, rep=rep, gen_s=round(gen, 2), size=size, **st)), flush=True)
         continue
     g = graph(name)
@@ -55,7 +56,7 @@ for name in a.cfgs:
     ws = W.Workspace(W.workspace_size(g.n, g.m, 1, W.options(a.layout)))
     for rep in range(a.reps):
         F, bm, st = W.maxflow(ro, col, cap, g.s, g.t, layout=a.layout, workspace=ws, gr_beta=a.beta,
-                              timeout_ms=100000, grid_blocks=a.blocks, push_mode=a.mode, gr_gamma=a.gamma, l2_persist=a.persist, bfs_mode=a.bfs, small_mode=a.small, gap_mode=a.gap)
+                              timeout_ms=100000, grid_blocks=a.blocks, push_mode=a.mode, gr_gamma=a.gamma, l2_persist=a.persist, bfs_mode=a.bfs, small_mode=a.small, gap_mode=a.gap, schedule=a.schedule)
         print(json.dumps(dict(cfg=name, rep=rep, gen_s=round(gen, 2), **st)), flush=True)
     if a.oracle:
         import oracle
