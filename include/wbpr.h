@@ -102,6 +102,10 @@ typedef struct wbpr_options {
                             active vertex (Alg. 2, the paper's method); 1: thread-centric -
                             every sweep one thread per vertex tests activity and scans the
                             residual arcs serially (Alg. 1 Step 1, the paper's baseline)     */
+  int32_t phase2;        /* 1: after the maximum preflow, return the stranded excess to the
+                            sources on the device (same loop, terminal roles swapped) so the
+                            residual state is a true flow; 0 (default): stop
+                            at the maximum preflow (flow value and cut are final there)     */
 } wbpr_options;
 
 typedef struct wbpr_stats {

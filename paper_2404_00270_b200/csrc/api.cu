@@ -309,6 +309,8 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.bfs_mode = opt.bfs_mode;
   P.small_mode = opt.small_mode;
   P.schedule = opt.schedule;
+  P.phase2 = opt.phase2;
+  P.h1 = at<int>(ws, L.h1);
   P.gr_gamma = opt.gr_gamma;
   P.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
   int occ = di.occ[opt.layout];
@@ -352,7 +354,11 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   if (bitmap && g->on_host) dbm = reinterpret_cast<uint32_t*>(at<int>(ws, L.q0));
   long long* d_flow = at<long long>(ws, L.inst_flow);
   long long* d_cut = at<long long>(ws, L.inst_cut);
-  extract_results(P, ro, col, cap, m, dbm, d_vb, k, d_flow, d_cut, di.num_sms, st);
+  {
+    SolveParams PX = P;
+    if (opt.phase2) PX.h = P.h1;   // the cut comes from the phase-1 labels
+    extract_results(PX, ro, col, cap, m, dbm, d_vb, k, d_flow, d_cut, di.num_sms, st);
+  }
   CK(cudaGetLastError());
   std::vector<long long> hf(k), hc(k);
   CK(cudaMemcpyAsync(hf.data(), d_flow, 8 * k, cudaMemcpyDeviceToHost, st));

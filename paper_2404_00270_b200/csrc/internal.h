@@ -122,7 +122,7 @@ struct Layout {
   int32_t layout;
   size_t ctrl, inst_s, inst_t, inst_flow, inst_cut, vbase;
   size_t in_row, in_col, in_cap;           // staging copy of a host CSR
-  size_t h, e, term, deact, deg, cursor, off, soff, roff, rsoff;
+  size_t h, e, term, deact, deg, cursor, off, soff, roff, rsoff, h1;
   size_t q0, q1, hq0, hq1, hc0, hc1, hist, hs;
   size_t scan_part;
   size_t regA, regB, regC;                 // build / residual regions
@@ -143,7 +143,7 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout) {
   L.inst_s = take(8 * k); L.inst_t = take(8 * k); L.inst_flow = take(8 * k); L.inst_cut = take(8 * k);
   L.vbase = take(8 * (k + 1));
   L.in_row = take(8 * (n + 1)); L.in_col = take(4 * m + 4); L.in_cap = take(4 * m + 4);
-  L.h = take(4 * n); L.e = take(8 * n); L.term = take(n); L.deact = take(n);
+  L.h = take(4 * n); L.e = take(8 * n); L.term = take(n); L.deact = take(n); L.h1 = take(4 * n);
   L.deg = take(4 * n + 4); L.cursor = take(4 * n + 4);
   L.off = take(4 * (n + 1)); L.soff = take(4 * (n + 1)); L.roff = take(4 * (n + 1)); L.rsoff = take(4 * (n + 1));
   L.q0 = take(4 * n + 4); L.q1 = take(4 * n + 4);
@@ -176,8 +176,10 @@ struct SolveParams {
   int* bcf;              // RCSR backward cf
   int* h;
   long long* e;
-  const uint8_t* term;
+  uint8_t* term;
   uint8_t* deact;
+  int* h1;               // phase-1 labels (the cut) saved before phase 2
+  int phase2;
   int* q[2];
   HugeRec* hq[2];
   int2* hc[2];

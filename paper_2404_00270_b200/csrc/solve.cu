@@ -163,6 +163,13 @@ struct SharedState {
 };
 
 // ------------------------------------------------------------------ warp append buffers
+// terminal flags change between the phases (phase 2 swaps them): plain coherent loads
+__device__ __forceinline__ uint8_t ld_term(const uint8_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
+  return (uint8_t)v;
+}
+
 struct QueueOut {   // next-queue destination
   int* q; int* qn;
   HugeRec* hq; int2* hc; int* hn; int* hc_cnt;
@@ -356,6 +363,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     return S.abort == 0;
   };
 
+  // targets of the global relabel: the sinks (phase 1) / the sources (phase 2)
+  const long long* SNK = P.snk;
   // ---------------------------------------------------------------- init
   if (blockIdx.x == 0 && threadIdx.x == 0) C->gap_level = N;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
             int dgv = dgc[j];
             ops.push(slot[j], dd);
             long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col[j]), (unsigned long long)dd);
-            if (!tc && old_v == 0 && __ldg(P.term + col[j]) == 0) small_append(col[j], dgv);
+            if (!tc && old_v == 0 && ld_term(P.term + col[j]) == 0) small_append(col[j], dgv);
             budget -= dd;
             pushed += dd;
             ++st_push;
@@ -481,7 +490,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-(long long)dd));
       long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + bcol), (unsigned long long)dd);
       if (!tc && old_u - dd > 0) small_append(u, d);
-      if (!tc && old_v == 0 && __ldg(P.term + bcol) == 0) small_append(bcol, dgv);
+      if (!tc && old_v == 0 && ld_term(P.term + bcol) == 0) small_append(bcol, dgv);
       ++st_push;
     } else if (P.push_mode != 0 && pushed > 0) {
       long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-pushed));
@@ -516,11 +525,14 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
   };
 
   enum { S_GR = 0, S_BFS = 1, S_COMPACT = 2, S_ROUND = 3, S_DONE = 4 };
+  int phase = 1;          // 2: return the stranded excess to the sources (NEXT #2)
+  bool converged = false; // phase ended by an exact GR with no active vertex
   long long rounds = 0;
   int cur = 0, fb = 0, level = 0;
   int state = S_GR;
   unsigned small_epoch = 0;
 
+  while (true) {
   while (state != S_DONE) {
     if (state == S_ROUND && (S.bc.flags & 8)) {   // (TC sweeps skip lifted vertices by h >= n)
       // ------------------------------------------------------------ gap lift (A6)
@@ -650,14 +662,14 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       // ------------------------------------------------------------ global relabel
       // reset labels: sinks 0, everything else |V| (= unreached); frontier <- sinks
       for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
-        st_cg(P.h + v, (__ldg(P.term + v) & kSink) ? 0 : ((__ldg(P.term + v) & kSource) ? N + 1 : N));
+        st_cg(P.h + v, (ld_term(P.term + v) & kSink) ? 0 : ((ld_term(P.term + v) & kSource) ? N + 1 : N));
         if (P.gap_mode) st_cg(P.hist + v, 0);
       }
       if (blockIdx.x == 0) {
         QueueOut o = out_for(0);
         for (int base = w * 32; base < P.k; base += kWarps * 32) {
           int i = base + lane;
-          int t = i < P.k ? (int)P.snk[i] : 0;
+          int t = i < P.k ? (int)SNK[i] : 0;
           int dg = i < P.k ? ops.degree(t) : 0;
           bool huge = i < P.k && dg > kChunk;
           if (huge) huge_append(t, dg, o);
@@ -825,13 +837,13 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           }
           if (v < N) {
             long long ev = ld_cg(P.e + v);
-            if (ev > 0 && __ldg(P.term + v) == 0) {
+            if (ev > 0 && ld_term(P.term + v) == 0) {
               int hv = ld_cg(P.h + v);
               if (hv < N) {
                 act = true;
                 dg = ops.degree(v);
                 huge = dg > kChunk;
-              } else if (!P.deact[v]) {
+              } else if (phase == 1 && !P.deact[v]) {
                 P.deact[v] = 1;
                 dropped += (unsigned long long)ev;
               }
@@ -853,6 +865,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       cur = 0;
       // termination: right after an exact GR, no active vertex <=> e(s)+e(t) >= Excess_total
       state = (S.bc.qn + S.bc.hc == 0) ? S_DONE : S_ROUND;
+      if (state == S_DONE) converged = true;
       continue;
     }
 
@@ -864,7 +877,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       unsigned long long active = 0;
       tc_work = 0;
       for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
-        if (ld_cg(P.e + v) > 0 && __ldg(P.term + v) == 0 && ld_cg(P.h + v) < N) {
+        if (ld_cg(P.e + v) > 0 && ld_term(P.term + v) == 0 && ld_cg(P.h + v) < N) {
           ++active;
           small_round_vertex(v, true);
         }
@@ -978,7 +991,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
             if (d > 0) {
               ops.push(slot, (int)d);
               long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col), (unsigned long long)d);
-              app = old_v == 0 && __ldg(P.term + col) == 0;
+              app = old_v == 0 && ld_term(P.term + col) == 0;
               ++st_push;
             }
             long long used = want < avail ? want : avail;
@@ -1034,7 +1047,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
             long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-(long long)d));
             long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + colv), (unsigned long long)d);
             if (old_u - d > 0) { app_u = u; dgu = sg.deg(); }
-            if (old_v == 0 && __ldg(P.term + colv) == 0) { app_v = colv; dgv = dv; }
+            if (old_v == 0 && ld_term(P.term + colv) == 0) { app_v = colv; dgv = dv; }
             ++st_push;
           } else if (P.push_mode != 0 && pushed > 0) {
             long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-pushed));
@@ -1070,6 +1083,25 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       // early break / periodic GR, decided by the barrier's last arriver
       if (S.bc.flags & 1) state = S_GR;
     }
+  }
+  // ---------------------------------------------------------------- phase 2 (NEXT #2)
+  // The maximum preflow is final: e(t) = F and the labels give S*.  Save them, swap the
+  // terminal roles and run the same loop toward the sources, which returns every
+  // stranded unit of excess to s through the residual arcs (a true flow).
+  if (phase == 1 && P.phase2 && converged) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
+      st_cg(P.h1 + v, ld_cg(P.h + v));
+      uint8_t tv = P.term[v];
+      P.term[v] = (uint8_t)(((tv & kSource) ? kSink : 0) | ((tv & kSink) ? kSource : 0));
+    }
+    SNK = P.src;
+    phase = 2;
+    converged = false;
+    state = S_GR;
+    if (!gsync()) return;
+    continue;
+  }
+  break;
   }
 
   // ---------------------------------------------------------------- statistics

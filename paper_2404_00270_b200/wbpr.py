@@ -44,7 +44,8 @@ class Options(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int32), ("gr_beta", ctypes.c_float), ("gap_mode", ctypes.c_int32),
                 ("max_rounds", ctypes.c_int64), ("grid_blocks", ctypes.c_int32), ("timeout_ms", ctypes.c_int32),
                 ("push_mode", ctypes.c_int32), ("gr_gamma", ctypes.c_float), ("l2_persist", ctypes.c_int32),
-                ("bfs_mode", ctypes.c_int32), ("small_mode", ctypes.c_int32), ("schedule", ctypes.c_int32)]
+                ("bfs_mode", ctypes.c_int32), ("small_mode", ctypes.c_int32), ("schedule", ctypes.c_int32),
+                ("phase2", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -112,7 +113,8 @@ def _check(st: int):
 def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: int = 0, grid_blocks: int = 0,
             timeout_ms: int = 0, push_mode: Optional[int] = None, gr_gamma: Optional[float] = None,
             l2_persist: Optional[int] = None, bfs_mode: Optional[int] = None,
-            small_mode: Optional[int] = None, schedule: Optional[str] = None) -> Options:
+            small_mode: Optional[int] = None, schedule: Optional[str] = None,
+            phase2: Optional[int] = None) -> Options:
     o = Options()
     _check(load().wbpr_default_options(ctypes.byref(o)))
     o.layout = _LAYOUTS[layout]
@@ -135,6 +137,8 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
         o.small_mode = small_mode
     if schedule is not None:
         o.schedule = {"vc": 0, "tc": 1, 0: 0, 1: 1}[schedule]
+    if phase2 is not None:
+        o.phase2 = phase2
     return o
 
 

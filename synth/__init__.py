@@ -61,6 +61,14 @@ def _L():
             lib.synth_select_hubs.restype = i32
             lib.synth_shuffle_rows.argtypes = [i64, P, P, P, u64]
             lib.synth_shuffle_rows.restype = None
+            lib.synth_rlg_count.argtypes = [i32, i32, i32]
+            lib.synth_rlg_count.restype = i64
+            lib.synth_rlg.argtypes = [i32, i32, i32, i32, u64, P, P, P]
+            lib.synth_rlg.restype = i64
+            lib.synth_genrmf_count.argtypes = [i32, i32]
+            lib.synth_genrmf_count.restype = i64
+            lib.synth_genrmf.argtypes = [i32, i32, i32, i32, u64, P, P, P]
+            lib.synth_genrmf.restype = i64
             lib.synth_draw.argtypes = [u64, u64, u64]
             lib.synth_draw.restype = u64
             _lib = lib
@@ -276,3 +284,28 @@ def c5_batch(count: int = 64, scale: int = 18, first_seed: int = 1000, rule: str
     """C5 instances [lo, hi) of the 64-instance batch: instance i uses seed first_seed+i."""
     hi = count if hi is None else hi
     return [rmat(scale, 16, first_seed + i, rule) for i in range(lo, hi)]
+
+
+# --------------------------------------------------------------------------- DIMACS-shaped (NEXT #4)
+def washington_rlg(levels: int = 512, width: int = 512, deg: int = 3, capmax: int = 10000, seed: int = 1) -> Graph:
+    """Washington random level graph (DIMACS 1st challenge shape, "S0"):
+    default 512 x 512 x 3 -> 262,146 vertices, 785,920 arcs."""
+    L = _L()
+    m = L.synth_rlg_count(levels, width, deg)
+    src, dst, cap = (np.empty(m, np.int32) for _ in range(3))
+    k = L.synth_rlg(levels, width, deg, capmax, seed, _p(src), _p(dst), _p(cap))
+    assert k == m
+    N = levels * width
+    return from_edges(N + 2, src, dst, cap, N, N + 1, name=f"rlg-{levels}x{width}x{deg}", config="S0")
+
+
+def genrmf(a: int = 128, b: int = 128, c1: int = 1, c2: int = 10000, seed: int = 1) -> Graph:
+    """Genrmf (DIMACS 1st challenge shape, PAPER.md P:414 "S1"): b frames of a x a grids;
+    default a = b = 128 -> 2,097,152 vertices, 10,403,840 arcs."""
+    L = _L()
+    m = L.synth_genrmf_count(a, b)
+    src, dst, cap = (np.empty(m, np.int32) for _ in range(3))
+    k = L.synth_genrmf(a, b, c1, c2, seed, _p(src), _p(dst), _p(cap))
+    assert k == m
+    n = a * a * b
+    return from_edges(n, src, dst, cap, 0, n - 1, name=f"genrmf-{a}x{b}", config="S1")

@@ -353,3 +353,70 @@ void synth_shuffle_rows(int64_t n, const int64_t* ro, int32_t* col, int32_t* cap
     }
   }
 }
+
+/* ---------- DIMACS-shaped generators (NEXT #4; structure decoded in SURVEY E1) ---------- */
+/* Washington random level graph: L levels of W vertices, each vertex -> `deg` random
+ * vertices of the next level, caps U[1, capmax]; S = L*W -> level 0, level L-1 -> T = L*W+1
+ * (super caps = incident sums).  Edge count = (L-1)*W*deg + 2*W. */
+int64_t synth_rlg_count(int32_t L, int32_t W, int32_t deg) { return (int64_t)(L - 1) * W * deg + 2ll * W; }
+int64_t synth_rlg(int32_t L, int32_t W, int32_t deg, int32_t capmax, uint64_t seed,
+                  int32_t* src, int32_t* dst, int32_t* cap) {
+  int64_t k = 0;
+  int32_t N = L * W;
+  for (int32_t l = 0; l + 1 < L; ++l)
+    for (int32_t x = 0; x < W; ++x)
+      for (int32_t d = 0; d < deg; ++d) {
+        uint64_t r = draw(seed, ST_EDGE, (uint64_t)k);
+        src[k] = l * W + x;
+        dst[k] = (l + 1) * W + (int32_t)(r % (uint64_t)W);
+        cap[k] = (int32_t)(1 + draw(seed, ST_CAP, (uint64_t)k) % (uint64_t)capmax);
+        ++k;
+      }
+  int64_t kin = k;
+  int64_t* outc = (int64_t*)calloc((size_t)N, sizeof(int64_t));
+  int64_t* inc = (int64_t*)calloc((size_t)N, sizeof(int64_t));
+  for (int64_t i = 0; i < kin; ++i) { outc[src[i]] += cap[i]; inc[dst[i]] += cap[i]; }
+  for (int32_t x = 0; x < W; ++x) { src[k] = N; dst[k] = x; cap[k] = (int32_t)(outc[x] ? outc[x] : 1); ++k; }
+  for (int32_t x = 0; x < W; ++x) {
+    int32_t v = (L - 1) * W + x;
+    src[k] = v; dst[k] = N + 1; cap[k] = (int32_t)(inc[v] ? inc[v] : 1); ++k;
+  }
+  free(outc); free(inc);
+  return k;
+}
+
+/* Genrmf (Goldfarb-Grigoriadis): b frames of a x a grids; in-frame 4-neighbour arcs (both
+ * directions) with cap c2*a*a; frame i -> frame i+1 through a seeded permutation with caps
+ * U[c1, c2]; s = vertex 0 of frame 0, t = last vertex of frame b-1.
+ * Edge count = 4*a*(a-1)*b + a*a*(b-1). */
+int64_t synth_genrmf_count(int32_t a, int32_t b) { return 4ll * a * (a - 1) * b + (int64_t)a * a * (b - 1); }
+int64_t synth_genrmf(int32_t a, int32_t b, int32_t c1, int32_t c2, uint64_t seed,
+                     int32_t* src, int32_t* dst, int32_t* cap) {
+  int64_t k = 0;
+  int32_t A = a * a;
+  int32_t big = c2 * a * a;
+  static const int dx[4] = {1, -1, 0, 0}, dy[4] = {0, 0, 1, -1};
+  for (int32_t f = 0; f < b; ++f)
+    for (int32_t y = 0; y < a; ++y)
+      for (int32_t x = 0; x < a; ++x)
+        for (int d = 0; d < 4; ++d) {
+          int32_t X = x + dx[d], Y = y + dy[d];
+          if (X < 0 || X >= a || Y < 0 || Y >= a) continue;
+          src[k] = f * A + y * a + x; dst[k] = f * A + Y * a + X; cap[k] = big; ++k;
+        }
+  int32_t* perm = (int32_t*)malloc((size_t)A * sizeof(int32_t));
+  for (int32_t f = 0; f + 1 < b; ++f) {
+    for (int32_t i = 0; i < A; ++i) perm[i] = i;
+    for (int32_t i = A - 1; i > 0; --i) {
+      int32_t j = (int32_t)(draw(seed, ST_PERM, (uint64_t)f * A + i) % (uint64_t)(i + 1));
+      int32_t t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+    }
+    for (int32_t i = 0; i < A; ++i) {
+      src[k] = f * A + i; dst[k] = (f + 1) * A + perm[i];
+      cap[k] = c1 + (int32_t)(draw(seed, ST_CAP, (uint64_t)k) % (uint64_t)(c2 - c1 + 1));
+      ++k;
+    }
+  }
+  free(perm);
+  return k;
+}

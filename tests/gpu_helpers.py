@@ -45,5 +45,6 @@ def assert_parity(g, layout="bcsr", ref=None, validate=True, **opt):
             f = check.demerge_bcsr(g.n, g.row_off, g.col, g.cap, R["off"], R["col"], R["cf"], R["cap0"], R["mate"])
         else:
             f = check.demerge_rcsr(g.n, g.row_off, g.col, g.cap, R["foff"], R["fcol"], R["fcf"], R["cap0"], R["bcf"])
-        check.check_flow(g.n, g.row_off, g.col, g.cap, g.s, g.t, F, bits_to_mask(words, g.n), f, strict=False)
+        check.check_flow(g.n, g.row_off, g.col, g.cap, g.s, g.t, F, bits_to_mask(words, g.n), f,
+                         strict=bool(opt.get("phase2", 0)))
     return F, st

@@ -266,3 +266,21 @@ def test_thread_centric(layout, push_mode):
     for g in (synth.rmat(12, 16, 7, "paper"), synth.rmat(11, 16, 3, "hub20"), synth.grid(30, 20, True, 1),
               synth.random_graph(600, 5000, 2, 0, 599), synth.tiny_random(10, 40, 6, 9)):
         assert_parity(g, layout, schedule="tc", push_mode=push_mode)
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_dimacs_shapes(layout):
+    for g in (synth.washington_rlg(64, 64, 3, 10000, 5), synth.genrmf(16, 16, 1, 10000, 5)):
+        assert_parity(g, layout)
+
+
+# ------------------------------------------------------------------ device phase 2 (NEXT #2)
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("schedule", ["vc", "tc"])
+def test_phase2_true_flow(layout, schedule):
+    # after phase 2 the de-merged residual state is a true flow: V2 strict conservation
+    gs = [synth.tiny_random(10, 40, 6, s) for s in range(20)]
+    gs += [synth.random_graph(1024, 8192, 4), synth.rmat(12, 16, 5, "hub20"), synth.grid(40, 30, True, 3),
+           synth.washington_rlg(30, 40, 3, 100, 1)]
+    for g in gs:
+        assert_parity(g, layout, phase2=1, schedule=schedule)

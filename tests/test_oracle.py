@@ -224,3 +224,20 @@ def test_bitmap_packing():
     r = oracle.OracleResult(0, 0, np.array([1, 0, 1] + [0] * 30 + [1], np.uint8), None, {}, 0.0)
     w = r.bitmap_words()
     assert w.dtype == np.uint32 and list(w) == [0b101, 0b10]
+
+
+# ------------------------------------------------------------------ DIMACS-shaped generators (NEXT #4)
+def test_dimacs_shapes_sizes():
+    # structure decoded from Table 1: Washington-RLG 512x512x3 and Genrmf a=b=128
+    g = synth.washington_rlg()
+    assert (g.n, g.m) == (262146, 785920)
+    L = synth._L()
+    assert (128 * 128 * 128, L.synth_genrmf_count(128, 128)) == (2097152, 10403840)
+
+
+@pytest.mark.parametrize("maker", [lambda: synth.washington_rlg(40, 50, 3, 100, 2), lambda: synth.genrmf(8, 10, 1, 100, 3)])
+def test_dimacs_shapes_vs_scipy(maker):
+    g = maker()
+    r = oracle.maxflow_graph(g)
+    assert r.flow == _scipy_flow(g) == r.cut_capacity
+    check.check_flow(g.n, g.row_off, g.col, g.cap, g.s, g.t, r.flow, r.in_S, r.edge_flow, strict=True)

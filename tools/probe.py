@@ -17,6 +17,8 @@ def graph(name):
     if name == "c3h": return synth.rmat(22, 16, 1, "hub20")
     if name == "r18p": return synth.rmat(18, 16, 1000, "paper")
     if name == "r18h": return synth.rmat(18, 16, 1000, "hub20")
+    if name == "rlg": return synth.washington_rlg()
+    if name == "genrmf": return synth.genrmf()
     if name.startswith("path"):
         k = int(name[4:])
         src = np.arange(k - 1); dst = src + 1
