@@ -106,6 +106,10 @@ typedef struct wbpr_options {
                             sources on the device (same loop, terminal roles swapped) so the
                             residual state is a true flow; 0 (default): stop
                             at the maximum preflow (flow value and cut are final there)     */
+  int32_t trace_rounds;  /* > 0: record one per-warp workload record (busy time, tasks, slots,
+                            pushes, relabels) for each of the first trace_rounds grid rounds
+                            (§4.3 Fig. 3; NEXT #3); the workspace grows
+                            by trace_rounds x 16384 x 32 B; read with wbpr_trace_view()     */
 } wbpr_options;
 
 typedef struct wbpr_stats {
@@ -205,6 +209,12 @@ wbpr_status wbpr_residual_view(const void* workspace, wbpr_residual* view);
  * tests (bit-exact against the definition). */
 wbpr_status wbpr_build_residual(const wbpr_csr* g, const wbpr_options* opt, void* workspace,
                                 size_t ws_bytes, wbpr_stats* stats, void* stream);
+
+/* Per-warp workload trace of the last solve in `workspace` (when trace_rounds > 0):
+ * *records = DEVICE pointer to 32-B records {int round, int warp, uint32 busy_ns, int tasks,
+ * int slots, int pushes, int relabels, int schedule} laid out [round][warp];
+ * *rounds = traced rounds, *warps = warps of the persistent grid. */
+wbpr_status wbpr_trace_view(const void* workspace, const void** records, int64_t* rounds, int32_t* warps);
 
 const char* wbpr_status_string(wbpr_status st);
 const char* wbpr_last_error(void);

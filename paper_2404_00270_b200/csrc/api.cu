@@ -42,6 +42,8 @@ struct DevInfo {
 std::mutex g_mu;
 std::unordered_map<int, DevInfo> g_dev;
 std::unordered_map<const void*, wbpr_residual> g_views;
+struct TraceInfo { const void* ptr; int rounds; int warps; };
+std::unordered_map<const void*, TraceInfo> g_traces;
 
 wbpr_status dev_info(DevInfo& out) {
   int dev = 0;
@@ -221,7 +223,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   }
   if (!ws) return fail(WBPR_EINVAL, "workspace is NULL");
   Ws W;
-  W.L = make_layout(n, m, k, opt.layout);
+  W.L = make_layout(n, m, k, opt.layout, opt.trace_rounds);
   if (ws_bytes < W.L.total)
     return fail(WBPR_ENOMEM, "workspace too small: need " + std::to_string(W.L.total) + " bytes");
   W.base = ws;
@@ -310,6 +312,8 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.small_mode = opt.small_mode;
   P.schedule = opt.schedule;
   P.phase2 = opt.phase2;
+  P.trace_rounds = opt.trace_rounds > 0 ? opt.trace_rounds : 0;
+  P.trace = P.trace_rounds ? at<TraceRec>(ws, L.trace) : nullptr;
   P.h1 = at<int>(ws, L.h1);
   P.gr_gamma = opt.gr_gamma;
   P.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
@@ -339,7 +343,12 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
       cudaGetLastError();
     }
   }
+  if (P.trace) CK(cudaMemsetAsync(P.trace, 0, sizeof(TraceRec) * (size_t)kTraceWarps * P.trace_rounds, st));
   CK(launch_solve(P, blocks, kSolveThreads, st));
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_traces[ws] = TraceInfo{P.trace, P.trace_rounds, blocks * (kSolveThreads / 32)};
+  }
   if (window) {
     cudaStreamAttrValue v{};
     v.accessPolicyWindow.num_bytes = 0;
@@ -444,7 +453,7 @@ wbpr_status wbpr_workspace_size(int64_t n, int64_t m, int32_t k, const wbpr_opti
   if (n < 2 || m < 0 || k < 1) return fail(WBPR_EINVAL, "bad sizes");
   if (n >= INT32_MAX || 2 * m >= INT32_MAX) return fail(WBPR_EOVERFLOW, "size beyond int32 indexing");
   wbpr_options o = resolve(opt);
-  *bytes = make_layout(n, m, k, o.layout).total;
+  *bytes = make_layout(n, m, k, o.layout, o.trace_rounds).total;
   return WBPR_OK;
 }
 
@@ -491,7 +500,7 @@ wbpr_status wbpr_bipartite_match(int64_t nL, int64_t nR, int64_t E, const int32_
   wbpr_options opt = resolve(opt_in);
   const int64_t n = nL + nR + 2, m = nL + E + nR;
   if (2 * m >= INT32_MAX || n >= INT32_MAX) return fail(WBPR_EOVERFLOW, "size beyond int32 indexing");
-  Layout L = make_layout(n, m, 1, opt.layout);
+  Layout L = make_layout(n, m, 1, opt.layout, opt.trace_rounds);
   if (ws_bytes < L.total) return fail(WBPR_ENOMEM, "workspace too small: need " + std::to_string(L.total) + " bytes");
   DevInfo di;
   wbpr_status s = dev_info(di);
@@ -542,6 +551,17 @@ wbpr_status wbpr_residual_view(const void* workspace, wbpr_residual* view) {
   auto it = g_views.find(workspace);
   if (it == g_views.end()) return fail(WBPR_EINVAL, "no residual has been built in this workspace");
   *view = it->second;
+  return WBPR_OK;
+}
+
+wbpr_status wbpr_trace_view(const void* workspace, const void** records, int64_t* rounds, int32_t* warps) {
+  if (!workspace || !records || !rounds || !warps) return fail(WBPR_EINVAL, "NULL argument");
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_traces.find(workspace);
+  if (it == g_traces.end() || !it->second.ptr) return fail(WBPR_EINVAL, "no traced solve in this workspace");
+  *records = it->second.ptr;
+  *rounds = it->second.rounds;
+  *warps = it->second.warps;
   return WBPR_OK;
 }
 

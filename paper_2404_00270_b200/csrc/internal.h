@@ -116,6 +116,15 @@ struct Ctrl {
   int gap_pending;        // the gap level the next lift phase uses
 };
 
+// Per-warp workload trace record (NEXT #3): one per warp per traced round.
+struct TraceRec {
+  int round, warp;
+  unsigned busy_ns;   // time from the round's start to the warp finishing its tasks
+  int tasks;          // queue tasks (VC) / active vertices (TC) the warp processed
+  int slots, pushes, relabels, schedule;
+};
+constexpr int kTraceWarps = 16384;   // trace capacity per round (>= any persistent grid)
+
 // Byte offsets of every region of a workspace (all 256-B aligned).
 struct Layout {
   int64_t n, m, k, H;       // H = 2m half-arcs (BCSR) ; RCSR uses m + m
@@ -126,13 +135,14 @@ struct Layout {
   size_t q0, q1, hq0, hq1, hc0, hc1, hist, hs;
   size_t scan_part;
   size_t regA, regB, regC;                 // build / residual regions
+  size_t trace;                            // per-warp trace records
   size_t bcap0;                            // offset inside regB of cap0
   size_t total;
 };
 
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
-inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout) {
+inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout, int32_t trace_rounds = 0) {
   Layout L{};
   L.n = n; L.m = m; L.k = k; L.layout = layout;
   L.H = 2 * m;
@@ -157,6 +167,7 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout) {
   L.regB = take(8 * H + 1024);
   L.bcap0 = align_up(4 * H + 260);
   L.regC = take(8 * H + 8);
+  L.trace = take(sizeof(TraceRec) * (size_t)kTraceWarps * (size_t)(trace_rounds > 0 ? trace_rounds : 0) + 32);
   L.total = o;
   return L;
 }
@@ -180,6 +191,8 @@ struct SolveParams {
   uint8_t* deact;
   int* h1;               // phase-1 labels (the cut) saved before phase 2
   int phase2;
+  TraceRec* trace;       // NEXT #3 per-warp trace (nullptr = off)
+  int trace_rounds;
   int* q[2];
   HugeRec* hq[2];
   int2* hc[2];

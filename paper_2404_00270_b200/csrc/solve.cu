@@ -418,6 +418,22 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     }
     if (nh < N) atomicAdd(P.hist + nh, 1);
   };
+  // per-warp workload trace (NEXT #3, §4.3 / Fig. 3): one record per warp per traced round
+  long long trace_round = 0;
+  auto trace_begin = [&](unsigned long long& t0, long long& a0, long long& p0, long long& r0, int& n0) {
+    t0 = globaltimer(); a0 = st_arcs; p0 = st_push; r0 = st_relabel; n0 = 0;
+  };
+  auto trace_end = [&](unsigned long long t0, long long a0, long long p0, long long r0, int ntasks) {
+    if (!P.trace || trace_round >= P.trace_rounds) return;
+    unsigned long long t1 = globaltimer();
+    long long da = warp_sum(st_arcs - a0), dp = warp_sum(st_push - p0), dr = warp_sum(st_relabel - r0);
+    if (lane_id() == 0) {
+      TraceRec r;
+      r.round = (int)trace_round; r.warp = gwarp; r.busy_ns = (unsigned)(t1 - t0); r.tasks = ntasks;
+      r.slots = (int)da; r.pushes = (int)dp; r.relabels = (int)dr; r.schedule = P.schedule;
+      P.trace[(long long)trace_round * nwarps + gwarp] = r;
+    }
+  };
   int sa = 0, sdst = 0;   // shared-memory queue being read; global queue buffer being written
   auto small_append = [&](int v, int dg) {
     if (dg > kChunk) {
@@ -876,12 +892,16 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       if (blockIdx.x == 0 && threadIdx.x == 0) { C->stats[ST_ROUNDS]++; ring(ph)->kind = PK_ROUND; }
       unsigned long long active = 0;
       tc_work = 0;
+      unsigned long long tt0; long long ta0, tp0, tr0c; int tn0;
+      trace_begin(tt0, ta0, tp0, tr0c, tn0);
       for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
         if (ld_cg(P.e + v) > 0 && ld_term(P.term + v) == 0 && ld_cg(P.h + v) < N) {
           ++active;
           small_round_vertex(v, true);
         }
       }
+      trace_end(tt0, ta0, tp0, tr0c, (int)warp_sum((int)active));
+      ++trace_round;
       if (lane == 0) st_cand += 0;
       unsigned long long ta = block_sum_u64(S, active);
       unsigned long long tw = block_sum_u64(S, tc_work);
@@ -914,7 +934,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       const int2* hcc = P.hc[cur];
       unsigned long long work = 0;
       const int total = qn + hc;
+      unsigned long long tt0; long long ta0, tp0, tr0c; int tn0;
+      trace_begin(tt0, ta0, tp0, tr0c, tn0);
       for (int tk = gwarp; tk < total; tk += nwarps) {
+        ++tn0;
         int u, lo, hi, hidx = -1;
         if (tk < qn) {
           u = ld_cg(qc + tk);
@@ -1067,6 +1090,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
         warp_append(S, cnt, lane == 0 && app_u >= 0, app_u, o, dgu);
         warp_append(S, cnt, lane == 0 && app_v >= 0, app_v, o, dgv);
       }
+      trace_end(tt0, ta0, tp0, tr0c, tn0);
+      ++trace_round;
       const unsigned long long tf0 = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer() : 0;
       block_flush_all(S, cnt, o);
       unsigned long long t = block_sum_u64(S, work);

@@ -24,7 +24,7 @@ _LAYOUTS = {"bcsr": 0, "rcsr": 1, 0: 0, 1: 1}
 EXPORTS = (
     "wbpr_default_options", "wbpr_workspace_size", "wbpr_maxflow_solve", "wbpr_maxflow_solve_batch",
     "wbpr_bipartite_workspace_size", "wbpr_bipartite_match", "wbpr_residual_view", "wbpr_build_residual",
-    "wbpr_status_string", "wbpr_last_error", "wbpr_version",
+    "wbpr_status_string", "wbpr_last_error", "wbpr_version", "wbpr_trace_view",
 )
 
 
@@ -45,7 +45,7 @@ class Options(ctypes.Structure):
                 ("max_rounds", ctypes.c_int64), ("grid_blocks", ctypes.c_int32), ("timeout_ms", ctypes.c_int32),
                 ("push_mode", ctypes.c_int32), ("gr_gamma", ctypes.c_float), ("l2_persist", ctypes.c_int32),
                 ("bfs_mode", ctypes.c_int32), ("small_mode", ctypes.c_int32), ("schedule", ctypes.c_int32),
-                ("phase2", ctypes.c_int32)]
+                ("phase2", ctypes.c_int32), ("trace_rounds", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -96,6 +96,9 @@ def load():
     for f in ("wbpr_default_options", "wbpr_workspace_size", "wbpr_maxflow_solve", "wbpr_maxflow_solve_batch",
               "wbpr_bipartite_workspace_size", "wbpr_bipartite_match", "wbpr_residual_view", "wbpr_build_residual"):
         getattr(lib, f).restype = ctypes.c_int32
+    lib.wbpr_trace_view.argtypes = [P, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(ctypes.c_int32)]
+    lib.wbpr_trace_view.restype = ctypes.c_int32
     lib.wbpr_status_string.argtypes = [i32]
     lib.wbpr_status_string.restype = ctypes.c_char_p
     lib.wbpr_last_error.restype = ctypes.c_char_p
@@ -114,7 +117,7 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
             timeout_ms: int = 0, push_mode: Optional[int] = None, gr_gamma: Optional[float] = None,
             l2_persist: Optional[int] = None, bfs_mode: Optional[int] = None,
             small_mode: Optional[int] = None, schedule: Optional[str] = None,
-            phase2: Optional[int] = None) -> Options:
+            phase2: Optional[int] = None, trace_rounds: Optional[int] = None) -> Options:
     o = Options()
     _check(load().wbpr_default_options(ctypes.byref(o)))
     o.layout = _LAYOUTS[layout]
@@ -139,6 +142,8 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
         o.schedule = {"vc": 0, "tc": 1, 0: 0, 1: 1}[schedule]
     if phase2 is not None:
         o.phase2 = phase2
+    if trace_rounds is not None:
+        o.trace_rounds = trace_rounds
     return o
 
 
@@ -319,6 +324,22 @@ def build_residual(row_off, col, cap, layout="bcsr", workspace: Optional[Workspa
         _check(L.wbpr_build_residual(ctypes.byref(c), ctypes.byref(o), ws.ptr, ws.nbytes, ctypes.byref(st),
                                      _stream_ptr(dev)))
     return residual(ws), st.as_dict()
+
+
+TRACE_DTYPE = np.dtype([("round", "<i4"), ("warp", "<i4"), ("busy_ns", "<u4"), ("tasks", "<i4"), ("slots", "<i4"),
+                        ("pushes", "<i4"), ("relabels", "<i4"), ("schedule", "<i4")])
+
+
+def trace(workspace: Workspace) -> np.ndarray:
+    """Per-warp workload records of the last traced solve: structured array [rounds, warps]."""
+    ptr = ctypes.c_void_p()
+    rounds = ctypes.c_int64()
+    warps = ctypes.c_int32()
+    _check(load().wbpr_trace_view(workspace.ptr, ctypes.byref(ptr), ctypes.byref(rounds), ctypes.byref(warps)))
+    off = ptr.value - workspace.tensor.data_ptr()
+    nbytes = rounds.value * warps.value * TRACE_DTYPE.itemsize
+    raw = workspace.tensor[off:off + nbytes].cpu().numpy()
+    return raw.view(TRACE_DTYPE).reshape(rounds.value, warps.value)
 
 
 def version() -> str:

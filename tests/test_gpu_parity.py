@@ -284,3 +284,29 @@ def test_phase2_true_flow(layout, schedule):
            synth.washington_rlg(30, 40, 3, 100, 1)]
     for g in gs:
         assert_parity(g, layout, phase2=1, schedule=schedule)
+
+
+# ------------------------------------------------------------------ workload trace (NEXT #3)
+def test_trace_vc_balances_better_than_tc():
+    # SPEC acceptance 5 analogue: on a skewed graph the vertex-centric schedule's
+    # mean-normalised per-warp busy-time spread is below the thread-centric one's
+    import torch
+    import paper_2404_00270_b200 as W
+    g = synth.rmat(14, 16, 3, "hub20")
+    ro, col, cap = to_dev(g)
+    spread = {}
+    for sch in ("tc", "vc"):
+        opt = W.options("bcsr", schedule=sch, trace_rounds=8, small_mode=0)
+        ws = W.Workspace(W.workspace_size(g.n, g.m, 1, opt))
+        F, _, st = W.maxflow(ro, col, cap, g.s, g.t, workspace=ws, schedule=sch, trace_rounds=8, small_mode=0)
+        rec = W.trace(ws)
+        assert rec.shape[0] == 8 and rec.shape[1] == st["grid_blocks"] * st["block_threads"] // 32
+        assert int(rec["pushes"].sum()) <= st["pushes"]
+        vals = []
+        for r in range(rec.shape[0]):
+            act = rec[r][rec[r]["tasks"] > 0]
+            if act.shape[0] > 1 and act["busy_ns"].mean() > 0:
+                b = act["busy_ns"].astype(float)
+                vals.append((b / b.mean()).std())
+        spread[sch] = float(np.median(vals))
+    assert spread["vc"] < spread["tc"], spread
