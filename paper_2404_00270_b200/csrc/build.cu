@@ -306,8 +306,7 @@ void build_bcsr(const BuildArgs& a, cudaStream_t st) {
 
 void build_bcsr_mate(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
-  // M is on the device (ctrl->M); H bounds it
-  { k_colcopy<<<grid_for(a.H, T, a.num_sms, 32), T, 0, st>>>(a.arc, a.ctrl, a.colv); note_launch(); }
+  // M is on the device (ctrl->M); H bounds it.  colv (dense columns) was written by the merge.
   int64_t threads = (a.H + kEdgesPerThread - 1) / kEdgesPerThread;
   if (a.H > 0) { k_mate<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.colv, (int)a.n, a.ctrl, a.mate, a.ctrl); note_launch(); }
 }
@@ -320,9 +319,10 @@ void build_rcsr_forward(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
   const int64_t n = a.n, m = a.m;
   { k_ro_to_i32<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.ro, n, a.soff); note_launch(); }
-  int64_t threads = (m + kEdgesPerThread - 1) / kEdgesPerThread;
-  if (m > 0) { k_keys_fwd<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, a.keys); note_launch(); }
-  segmented_sort(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.ctrl, a.arc, a.arc + a.H / 2, a.q0, a.num_sms, st);
+  // rows already column-sorted in the input are not sorted again
+  outkeys_need(a, a.keys, st);
+  segmented_sort_filtered(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.need, a.ctrl, a.arc, a.arc + a.H / 2, a.q0,
+                          a.num_sms, st);
   int* flags = (int*)a.tmp;
   cudaMemsetAsync(flags, 0, sizeof(int) * (m + 1), st);
   { k_rowstarts<<<grid_for(n, T, a.num_sms), T, 0, st>>>(a.soff, n, flags); note_launch(); }

@@ -84,6 +84,7 @@ struct MergeArgs {
   const int* off;           // pass 1 input: final offsets
   int2* arc;                // pass 1 output
   int* cap0;
+  int* colv;                // pass 1 output: dense column copy for the mate search
   int* wlist;               // vertices for the warp class
   int2* tasks;              // (vertex, chunk) tasks of the chunked class (> kMergeWarpMax)
   int* chunk_heads;         // distinct columns found by each chunk task
@@ -94,6 +95,7 @@ __device__ __forceinline__ void emit(const MergeArgs& a, int slot, uint32_t c, l
   if (sum > INT_MAX) { atomicExch(&a.ctrl->overflow, 1); sum = INT_MAX; }
   a.arc[slot] = make_int2((int)c, (int)sum);
   a.cap0[slot] = (int)sum;
+  a.colv[slot] = (int)c;
 }
 
 template <int PASS>
@@ -275,6 +277,14 @@ static unsigned gridcap(int64_t items, int threads, int num_sms, int per_sm) {
   return (unsigned)(b < 1 ? 1 : b);
 }
 
+// 64-bit row keys in input order + per-row "needs sorting" flags (also used by RCSR).
+void outkeys_need(const BuildArgs& a, uint64_t* keys, cudaStream_t st) {
+  const int T = 256;
+  cudaMemsetAsync(a.need, 0, a.n, st);
+  int64_t threads = (a.m + 7) / 8;
+  if (a.m > 0) { k_outkeys<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(a.ro, a.col, a.cap, a.n, a.m, keys, a.need); note_launch(); }
+}
+
 // Build BCSR from the validated input (BuildArgs: deg = in-degrees, maxlen = max
 // in-degree, maxlen_out = max out-degree).
 void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
@@ -302,7 +312,7 @@ void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
   segmented_sort32(ink, itmp, a.rsoff, (int)n, a.maxlen, a.ctrl, items, items_med, a.q0, a.num_sms, st);
   MergeArgs ma;
   ma.ooff = a.soff; ma.outk = outk; ma.ioff = a.rsoff; ma.ink = ink; ma.n = (int)n;
-  ma.mdeg = a.deg; ma.off = a.off; ma.arc = a.arc; ma.cap0 = a.cap0;
+  ma.mdeg = a.deg; ma.off = a.off; ma.arc = a.arc; ma.cap0 = a.cap0; ma.colv = a.colv;
   ma.wlist = a.q0; ma.tasks = a.mtasks; ma.chunk_heads = a.mheads; ma.ctrl = a.ctrl;
   cudaMemsetAsync(&a.ctrl->mlist_w, 0, 2 * sizeof(int), st);
   { k_merge_thread<0><<<gridcap(n, T, a.num_sms, 16), T, 0, st>>>(ma); note_launch(); }

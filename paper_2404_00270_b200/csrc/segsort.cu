@@ -28,22 +28,30 @@ template <typename K> __device__ __forceinline__ K key_max() { return (K)~(K)0; 
 template <typename K>
 __global__ void __launch_bounds__(256) k_sort_warp(K* keys, const int* __restrict__ off, int nseg,
                                                    const uint8_t* __restrict__ need) {
+  // each warp screens 32 consecutive segments with one ballot, then rank-sorts the ones
+  // with 2..32 keys (and a set `need` flag) one after the other
   int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = lane_id();
   int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int sgi = wg; sgi < nseg; sgi += nw) {
-    if (need && !need[sgi]) continue;
-    int beg = off[sgi], len = off[sgi + 1] - beg;
-    if (len < 2 || len > 32) continue;
-    K k = lane < len ? keys[beg + lane] : key_max<K>();
-    int rank = 0;
+  for (int base = wg * 32; base < nseg; base += nw * 32) {
+    int sgi = base + lane;
+    int beg = 0, len = 0;
+    if (sgi < nseg && (!need || need[sgi])) { beg = off[sgi]; len = off[sgi + 1] - beg; }
+    unsigned todo = __ballot_sync(FULL, len >= 2 && len <= 32);
+    while (todo) {
+      int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      int b = __shfl_sync(FULL, beg, j), l = __shfl_sync(FULL, len, j);
+      K k = lane < l ? keys[b + lane] : key_max<K>();
+      int rank = 0;
 #pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
-      K o = __shfl_sync(FULL, k, j);
-      rank += (o < k) || (o == k && j < lane);
+      for (int q = 0; q < 32; ++q) {
+        K o = __shfl_sync(FULL, k, q);
+        rank += (o < k) || (o == k && q < lane);
+      }
+      __syncwarp();
+      if (lane < l) keys[b + rank] = k;
     }
-    __syncwarp();
-    if (lane < len) keys[beg + rank] = k;
   }
 }
 
@@ -245,8 +253,8 @@ void segmented_sort_t(K* keys, K* tmp, const int* off, int nseg, int maxlen, con
   cudaMemsetAsync(&ctrl->sort_items_med, 0, sizeof(int), st);
   cudaMemsetAsync(&ctrl->hub_chunks, 0, sizeof(int), st);
   {
-    int64_t blocks = ((int64_t)nseg * 32 + 255) / 256;
-    if (blocks > (int64_t)num_sms * 64) blocks = (int64_t)num_sms * 64;
+    int64_t blocks = ((int64_t)nseg + 255) / 256;
+    if (blocks > (int64_t)num_sms * 32) blocks = (int64_t)num_sms * 32;
     { k_sort_warp<K><<<(unsigned)blocks, 256, 0, st>>>(keys, off, nseg, need); note_launch(); }
   }
   if (maxlen <= 32) return;

@@ -43,6 +43,21 @@ ap.add_argument("--oracle", action="store_true")
 a = ap.parse_args()
 for name in a.cfgs:
     t0 = time.time()
+    if name == "c5":
+        B = synth.disjoint_union(synth.c5_batch())
+        G = B.union
+        ro, col, cap = (torch.from_numpy(x).cuda() for x in (G.row_off, G.col, G.cap))
+        opt = W.options(a.layout)
+        ws = W.Workspace(W.workspace_size(G.n, G.m, 64, opt))
+        gen = time.time() - t0
+        for rep in range(a.reps):
+            flows, cuts, bm, st = W.maxflow_batch(ro, col, cap, B.vbase, B.s, B.t, layout=a.layout, workspace=ws,
+                                                  gr_beta=a.beta, timeout_ms=100000, grid_blocks=a.blocks,
+                                                  push_mode=a.mode, gr_gamma=a.gamma, l2_persist=a.persist,
+                                                  bfs_mode=a.bfs, small_mode=a.small, gap_mode=a.gap,
+                                                  schedule=a.schedule)
+            print(json.dumps(dict(cfg=name, rep=rep, gen_s=round(gen, 2), **st)), flush=True)
+        continue
     if name == "c4":
         l, r = synth.bipartite_edges()
         lt, rt = torch.from_numpy(l).cuda(), torch.from_numpy(r).cuda()
