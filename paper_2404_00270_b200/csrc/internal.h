@@ -50,6 +50,7 @@ struct GrPolicy {
   unsigned long long t_after_gr;
   unsigned long long gr_time;
   unsigned long long bfs_seen_edges;   // slots of the vertices labelled so far in this GR
+  unsigned long long prev_reached;     // slots labelled by the previous GR (0 = none yet)
   int bfs_bottom_up;                   // direction of the current BFS level
   int pad;
 };

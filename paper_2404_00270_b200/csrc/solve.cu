@@ -312,7 +312,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           const unsigned long long fe = ld_cg(&r->fedges);
           if (kind == PK_GR_RESET) { G.bfs_seen_edges = 0; G.bfs_bottom_up = 0; }
           G.bfs_seen_edges += fe;
-          const unsigned long long Mtot = (unsigned long long)Mslots;
+          // slots still to be labelled: bounded by what the previous GR reached (vertices cut
+          // off from the sinks stay unreachable, N5), so large unreachable regions do not
+          // pull the BFS into bottom-up scans that can never find a parent
+          unsigned long long Mtot = (unsigned long long)Mslots;
+          if (G.prev_reached && G.prev_reached < Mtot) Mtot = G.prev_reached;
           const unsigned long long rest = Mtot > G.bfs_seen_edges ? Mtot - G.bfs_seen_edges : 0;
           if (!G.bfs_bottom_up) G.bfs_bottom_up = P.bfs_mode != 0 && fe * 14ull > rest;
           else G.bfs_bottom_up = (long long)qn * 24 >= (long long)N;
@@ -320,6 +324,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           if (G.bfs_bottom_up) flags |= 2;
         } else if (kind == PK_COMPACT) {
           C->gap_level = N;
+          G.prev_reached = G.bfs_seen_edges;
           G.gr_time = now - G.t_gr_start;
           G.t_after_gr = now;
           G.work_since_gr = 0;
