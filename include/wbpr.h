@@ -110,6 +110,13 @@ typedef struct wbpr_options {
                             pushes, relabels) for each of the first trace_rounds grid rounds
                             (§4.3 Fig. 3; NEXT #3); the workspace grows
                             by trace_rounds x 16384 x 32 B; read with wbpr_trace_view()     */
+  int32_t batch_groups;  /* batch solves (A10): number of independent solver groups the
+                            persistent grid is split into (contiguous instance ranges, CTAs
+                            proportional to edges, each with its own barrier, queues and GR
+                            policy); 0 or 1 (default) = one solver for the whole disjoint
+                            union (it shares the grid dynamically: on C5 the groups' static
+                            CTA shares leave the easy groups' CTAs idle behind the hardest
+                            instance, profiles/r1)                                           */
 } wbpr_options;
 
 typedef struct wbpr_stats {

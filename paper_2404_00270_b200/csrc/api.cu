@@ -233,6 +233,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   if (s) return s;
   const Layout& L = W.L;
 
+  if (opt.batch_groups < 0) return fail(WBPR_EINVAL, "batch_groups must be >= 0");
   const long long launches0 = launch_count();
   Events E;
   CK(E.create());
@@ -321,6 +322,74 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   if (occ < 1) return fail(WBPR_ECUDA, "solve kernel cannot be resident on this device");
   int blocks = di.num_sms * occ;
   if (opt.grid_blocks > 0 && opt.grid_blocks < blocks) blocks = opt.grid_blocks;
+
+  // ---- solver groups (A10): independent instances get disjoint CTA groups of the
+  // persistent grid, sized by their edge counts, each with its own barrier and state
+  std::vector<GroupDesc> groups;
+  {
+    int G = 1;
+    if (k > 1) {
+      G = opt.batch_groups > 0 ? opt.batch_groups : 1;
+      G = std::max(1, std::min(G, std::min(k, std::min(blocks, kMaxGroups))));
+    }
+    std::vector<int64_t> eoff(k + 1, 0);
+    if (G > 1) {
+      // edge offsets at the instance boundaries: row_offsets[vbase[i]]
+      if (g->on_host) {
+        for (int i = 0; i <= k; ++i) eoff[i] = g->row_offsets[vbase_h[i]];
+      } else {
+        for (int i = 0; i <= k; ++i)
+          CK(cudaMemcpyAsync(&eoff[i], ro + vbase_h[i], 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+    }
+    const int64_t mtot = std::max<int64_t>(1, eoff[k] - eoff[0]);
+    // contiguous instance ranges with balanced edge counts
+    std::vector<int> cut(G + 1, 0);
+    cut[G] = k;
+    for (int gi = 1; gi < G; ++gi) {
+      int64_t target = eoff[0] + mtot * gi / G;
+      int i = cut[gi - 1] + 1;
+      while (i < k - (G - gi) && eoff[i] < target) ++i;
+      cut[gi] = i;
+    }
+    // CTAs proportional to edges, at least one per group
+    std::vector<int> nbg(G, 1);
+    int left = blocks - G;
+    std::vector<std::pair<double, int>> rem;
+    for (int gi = 0; gi < G; ++gi) {
+      double share = (G == 1) ? blocks : (double)left * (double)(eoff[cut[gi + 1]] - eoff[cut[gi]]) / (double)mtot;
+      int add = G == 1 ? blocks - 1 : (int)share;
+      nbg[gi] += add;
+      rem.push_back({share - add, gi});
+    }
+    int used = 0;
+    for (int gi = 0; gi < G; ++gi) used += nbg[gi];
+    std::sort(rem.begin(), rem.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    for (int r = 0; used < blocks && r < (int)rem.size(); ++r, ++used) nbg[rem[r].second]++;
+    int b0 = 0;
+    int64_t hub0 = 0;
+    for (int gi = 0; gi < G; ++gi) {
+      GroupDesc d{};
+      d.b0 = b0; d.nb = nbg[gi]; d.i0 = cut[gi]; d.i1 = cut[gi + 1];
+      d.vlo = (int)vbase_h[d.i0]; d.vhi = (int)vbase_h[d.i1]; d.hub0 = (int)hub0;
+      const int64_t mg = G == 1 ? m : eoff[d.i1] - eoff[d.i0];
+      hub0 += 2 * mg / kChunk + 64;
+      b0 += d.nb;
+      groups.push_back(d);
+    }
+    blocks = b0;
+    CK(cudaMemcpyAsync(at<GroupDesc>(ws, L.gdesc), groups.data(), sizeof(GroupDesc) * groups.size(),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(at<GroupCtrl>(ws, L.gctrl), 0, sizeof(GroupCtrl) * groups.size(), st));
+    P.groups = at<GroupDesc>(ws, L.gdesc);
+    P.gctrl = at<GroupCtrl>(ws, L.gctrl);
+    P.ngroups = (int)groups.size();
+    if (P.ngroups > 1) {
+      P.trace = nullptr; P.trace_rounds = 0;
+      P.gap_mode = 0;   // the online gap histogram is indexed by height: one solver only
+    }
+  }
   // Keep the label array h[] (the random-gather target of every scan and BFS step)
   // resident in L2: a persisting access-policy window over h for the solve launch.
   bool window = false;
@@ -445,6 +514,7 @@ wbpr_status wbpr_default_options(wbpr_options* opt) {
   opt->l2_persist = 0;
   opt->bfs_mode = 1;
   opt->small_mode = 1;
+  opt->batch_groups = 0;
   return WBPR_OK;
 }
 

@@ -85,17 +85,36 @@ struct Resume {
   long long rounds;
 };
 
-// Device control block at the start of the workspace.
-struct Ctrl {
+// Per-group solver state (A10): every solver group (one instance, several instances,
+// or the whole batch) has its own barrier, phase counters, GR policy and hand-off record.
+struct GroupCtrl {
   GridBarrier bar;
   int pad_bar[2];
   Bcast bc;
-  int abort;
-  int status;
   Ring ring[3];
   GrPolicy pol;
   Resume res;
   int small_hn, small_hc;  // huge appends made in the small mode
+  int gap_level;           // online gap: lowest emptied level seen since the last check (A6)
+  int gap_pending;         // the gap level the next lift phase uses
+  int nhs;                 // entries of the static huge-chunk list
+  int pad[3];
+};
+
+// Host-computed partition of the persistent grid into solver groups.
+struct GroupDesc {
+  int b0, nb;     // CTAs [b0, b0 + nb)
+  int i0, i1;     // instances [i0, i1)
+  int vlo, vhi;   // vertices [vlo, vhi)
+  int hub0;       // offset of the group's slice of the huge-vertex arrays
+  int pad;
+};
+constexpr int kMaxGroups = 1024;
+
+// Device control block at the start of the workspace.
+struct Ctrl {
+  int abort;
+  int status;
   long long excess_total;
   long long stats[ST_COUNT];
   // build info
@@ -111,10 +130,7 @@ struct Ctrl {
   int sort_items_med;     // build scratch counter
   int mlist_w, mlist_c;   // build: vertices merged by a warp / by a CTA
   int maxlen_out;         // build: longest input row
-  int nhs;                // solve: entries of the static huge-chunk list
   int pad0[1];
-  int gap_level;          // online gap: lowest emptied level seen since the last check (A6)
-  int gap_pending;        // the gap level the next lift phase uses
 };
 
 // Per-warp workload trace record (NEXT #3): one per warp per traced round.
@@ -137,6 +153,7 @@ struct Layout {
   size_t scan_part;
   size_t regA, regB, regC;                 // build / residual regions
   size_t trace;                            // per-warp trace records
+  size_t gdesc, gctrl;                     // solver groups
   size_t bcap0;                            // offset inside regB of cap0
   size_t total;
 };
@@ -158,7 +175,7 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout, int32
   L.deg = take(4 * n + 4); L.cursor = take(4 * n + 4);
   L.off = take(4 * (n + 1)); L.soff = take(4 * (n + 1)); L.roff = take(4 * (n + 1)); L.rsoff = take(4 * (n + 1));
   L.q0 = take(4 * n + 4); L.q1 = take(4 * n + 4);
-  int64_t hub = H / kChunk + 64;
+  int64_t hub = H / kChunk + 64 * (k + 1);   // per-group slices (+64 slack each)
   L.hq0 = take(sizeof(HugeRec) * hub); L.hq1 = take(sizeof(HugeRec) * hub);
   L.hc0 = take(8 * (2 * hub + 64)); L.hc1 = take(8 * (2 * hub + 64));
   L.hist = take(4 * (n + 2));
@@ -169,6 +186,8 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout, int32
   L.bcap0 = align_up(4 * H + 260);
   L.regC = take(8 * H + 8);
   L.trace = take(sizeof(TraceRec) * (size_t)kTraceWarps * (size_t)(trace_rounds > 0 ? trace_rounds : 0) + 32);
+  L.gdesc = take(sizeof(GroupDesc) * kMaxGroups);
+  L.gctrl = take(sizeof(GroupCtrl) * kMaxGroups);
   L.total = o;
   return L;
 }
@@ -194,6 +213,9 @@ struct SolveParams {
   int phase2;
   TraceRec* trace;       // NEXT #3 per-warp trace (nullptr = off)
   int trace_rounds;
+  const GroupDesc* groups;   // solver groups (sorted by b0)
+  GroupCtrl* gctrl;
+  int ngroups;
   int* q[2];
   HugeRec* hq[2];
   int2* hc[2];

@@ -251,14 +251,33 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
   ops.init();
   const unsigned long long pl = policy_evict_last();   // keep h[] in L2
   Ctrl* C = P.ctrl;
-  const int N = P.n;
-  const int Mslots = P.layout == 0 ? ld_cg((const int*)&C->M) : 2 * P.Mf;
+  const int N = P.n;                 // |V| of the union: the label bound (h >= N: inactive)
+  // ---- solver group of this CTA (A10 batches): CTAs [b0, b0+nb) run an independent
+  // solver over instances [I0, I1) = vertices [VLO, VHI) with their own barrier, counters,
+  // queues and GR policy; a single instance is one group spanning the whole grid
+  int gid = 0;
+  {
+    int lo = 0, hi = P.ngroups;
+    while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (P.groups[mid].b0 <= (int)blockIdx.x) lo = mid; else hi = mid; }
+    gid = lo;
+  }
+  const GroupDesc GD = P.groups[gid];
+  GroupCtrl* GC = P.gctrl + gid;
+  const int brank = (int)blockIdx.x - GD.b0;   // CTA rank inside the group
+  const unsigned nb = (unsigned)GD.nb;
+  const int VLO = GD.vlo, VHI = GD.vhi, I0 = GD.i0, KI = GD.i1 - GD.i0;
+  int* const Q[2] = {P.q[0] + VLO, P.q[1] + VLO};
+  HugeRec* const HQ[2] = {P.hq[0] + GD.hub0, P.hq[1] + GD.hub0};
+  int2* const HC[2] = {P.hc[0] + 2 * GD.hub0, P.hc[1] + 2 * GD.hub0};
+  int2* const HS = P.hs + 2 * GD.hub0;
+  const int Mslots = P.layout == 0 ? (__ldg(P.off + VHI) - __ldg(P.off + VLO))
+                                   : 2 * (__ldg(P.off + VHI) - __ldg(P.off + VLO));
   const unsigned long long gr_threshold =
-      (unsigned long long)((double)P.gr_beta * (double)((long long)N + (long long)ld_cg((const int*)&C->M))) + 1;
-  const unsigned nb = gridDim.x;
+      (unsigned long long)((double)P.gr_beta * (double)((long long)(VHI - VLO) + (long long)Mslots)) + 1;
   const int lane = lane_id(), w = warp_id();
-  const int gwarp = blockIdx.x * kWarps + w;
-  const int nwarps = gridDim.x * kWarps;
+  const int gwarp = brank * kWarps + w;
+  const int nwarps = (int)nb * kWarps;
+  long long l_rounds = 0, l_grs = 0, l_levels = 0;   // thread 0 of CTA rank 0: per-group counts
   unsigned gen = 0;
   int ph = 0;
   const unsigned long long deadline = globaltimer() + P.deadline_ns_rel;
@@ -266,30 +285,30 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
   long long st_push = 0, st_relabel = 0, st_arcs = 0, st_bfs_arcs = 0, st_cand = 0;
   int cnt = 0;  // this warp's staged appends (lane-uniform)
 
-  auto ring = [&](int p) -> Ring* { return &C->ring[p % 3]; };
+  auto ring = [&](int p) -> Ring* { return &GC->ring[p % 3]; };
   auto out_for = [&](int buf) {
     QueueOut o;
     Ring* r = ring(ph);
-    o.q = P.q[buf]; o.qn = &r->qn;
-    o.hq = P.hq[buf]; o.hc = P.hc[buf]; o.hn = &r->hn; o.hc_cnt = &r->hc;
+    o.q = Q[buf]; o.qn = &r->qn;
+    o.hq = HQ[buf]; o.hc = HC[buf]; o.hn = &r->hn; o.hc_cnt = &r->hc;
     o.md = &r->maxdeg;
     return o;
   };
   unsigned long long t_sync = 0, t_flush = 0, t_round = 0;
   auto gsync = [&]() -> bool {
-    const unsigned long long ts0 = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer() : 0;
+    const unsigned long long ts0 = (brank == 0 && threadIdx.x == 0) ? globaltimer() : 0;
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned target = gen + 1;
       int ab = 0;
       uint4 b;
-      unsigned old = atom_add_acqrel(&C->bar.count, 1u);
+      unsigned old = atom_add_acqrel(&GC->bar.count, 1u);
       if (old == nb - 1) {
-        C->bar.count = 0;
+        GC->bar.count = 0;
         Ring* r = ring(ph);
         const int qn = ld_cg(&r->qn), hc = ld_cg(&r->hc), kind = ld_cg(&r->kind);
         const unsigned long long now = globaltimer();
-        GrPolicy& G = C->pol;
+        GrPolicy& G = GC->pol;
         unsigned flags = 0;
         if (kind == PK_ROUND) {
           atomicAdd((unsigned long long*)&C->stats[ST_AVQ], (unsigned long long)(qn + ld_cg(&r->hn)));
@@ -300,8 +319,8 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
                      (P.gr_gamma > 0.f && (double)(now - G.t_after_gr) >= (double)P.gr_gamma * (double)G.gr_time);
           if (due) { flags = 1; G.t_gr_start = now; }
           else if (P.gap_mode) {
-            const int gl = ld_cg(&C->gap_level);
-            if (gl < N) { flags |= 8; C->gap_pending = gl; C->gap_level = N; }
+            const int gl = ld_cg(&GC->gap_level);
+            if (gl < N) { flags |= 8; GC->gap_pending = gl; GC->gap_level = N; }
           }
         } else if (kind == PK_PREFLOW) {
           G.t_gr_start = now;
@@ -319,11 +338,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           if (G.prev_reached && G.prev_reached < Mtot) Mtot = G.prev_reached;
           const unsigned long long rest = Mtot > G.bfs_seen_edges ? Mtot - G.bfs_seen_edges : 0;
           if (!G.bfs_bottom_up) G.bfs_bottom_up = P.bfs_mode != 0 && fe * 14ull > rest;
-          else G.bfs_bottom_up = (long long)qn * 24 >= (long long)N;
+          else G.bfs_bottom_up = (long long)qn * 24 >= (long long)(VHI - VLO);
           if (P.bfs_mode == 2) G.bfs_bottom_up = 1;
           if (G.bfs_bottom_up) flags |= 2;
         } else if (kind == PK_COMPACT) {
-          C->gap_level = N;
+          GC->gap_level = N;
           G.prev_reached = G.bfs_seen_edges;
           G.gr_time = now - G.t_gr_start;
           G.t_after_gr = now;
@@ -345,11 +364,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
         b.w = flags;
         Ring* z = ring(ph + 1);
         z->qn = 0; z->hn = 0; z->hc = 0; z->work = 0; z->kind = 0; z->fedges = 0; z->maxdeg = 0;
-        st_release_v4(&C->bc, b);
+        st_release_v4(&GC->bc, b);
       } else {
         unsigned ns = 0;
         while (true) {
-          b = ld_acquire_v4(&C->bc);
+          b = ld_acquire_v4(&GC->bc);
           if (b.x == target) break;
           if (ld_volatile(&C->abort)) { ab = 1; break; }
           if (globaltimer() > deadline) { atomicExch(&C->abort, 1); ab = 1; break; }
@@ -364,23 +383,23 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     ++gen;
     ++ph;
     __syncthreads();
-    if (blockIdx.x == 0 && threadIdx.x == 0) t_sync += globaltimer() - ts0;
+    if (brank == 0 && threadIdx.x == 0) t_sync += globaltimer() - ts0;
     return S.abort == 0;
   };
 
   // targets of the global relabel: the sinks (phase 1) / the sources (phase 2)
-  const long long* SNK = P.snk;
+  const long long* SNK = P.snk + I0;
   // ---------------------------------------------------------------- init
-  if (blockIdx.x == 0 && threadIdx.x == 0) C->gap_level = N;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
+  if (brank == 0 && threadIdx.x == 0) GC->gap_level = N;
+  for (int v = VLO + brank * blockDim.x + threadIdx.x; v < VHI; v += nb * blockDim.x) {
     st_cg(P.e + v, 0ll);
     P.deact[v] = 0;
     // static chunk list of the vertices with > kChunk slots (bottom-up BFS splits them)
     int dg = ops.degree(v);
     if (dg > kChunk) {
       int nch = (dg + kChunk - 1) / kChunk;
-      int t0 = atomicAdd(&C->nhs, nch);
-      for (int j = 0; j < nch; ++j) P.hs[t0 + j] = make_int2(v, j);
+      int t0 = atomicAdd(&GC->nhs, nch);
+      for (int j = 0; j < nch; ++j) HS[t0 + j] = make_int2(v, j);
     }
   }
   if (!gsync()) return;
@@ -388,11 +407,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
   // ---------------------------------------------------------------- preflow (Alg. 1 Step 0)
   {
     unsigned long long exc = 0;
-    for (int i = 0; i < P.k; ++i) {
+    for (int i = I0; i < I0 + KI; ++i) {
       int s = (int)P.src[i];
       Seg sg = ops.seg(s);
       int d = sg.deg();
-      for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d; j += nb * blockDim.x) {
+      for (int j = brank * blockDim.x + threadIdx.x; j < d; j += nb * blockDim.x) {
         int col, cf, slot;
         ops.out_arc(sg, j, col, cf, slot);
         if (cf > 0) {   // c_f(s,v) <- 0, c_f(v,s) <- c(s,v), e(v) <- c(s,v)
@@ -404,7 +423,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     }
     unsigned long long t = block_sum_u64(S, exc);
     if (threadIdx.x == 0 && t) atomicAdd((unsigned long long*)&C->excess_total, t);
-    if (blockIdx.x == 0 && threadIdx.x == 0) ring(ph)->kind = PK_PREFLOW;
+    if (brank == 0 && threadIdx.x == 0) ring(ph)->kind = PK_PREFLOW;
   }
   if (!gsync()) return;
 
@@ -419,7 +438,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     if (!P.gap_mode) return;
     if (old < N) {
       int prev = atomicSub(P.hist + old, 1);
-      if (prev == 1) atomicMin(&C->gap_level, old);
+      if (prev == 1) atomicMin(&GC->gap_level, old);
     }
     if (nh < N) atomicAdd(P.hist + nh, 1);
   };
@@ -444,13 +463,13 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     if (dg > kChunk) {
       QueueOut ho;
       ho.q = nullptr; ho.qn = nullptr; ho.md = nullptr;
-      ho.hq = P.hq[sdst]; ho.hc = P.hc[sdst]; ho.hn = &C->small_hn; ho.hc_cnt = &C->small_hc;
+      ho.hq = HQ[sdst]; ho.hc = HC[sdst]; ho.hn = &GC->small_hn; ho.hc_cnt = &GC->small_hc;
       huge_append(v, dg, ho);
       S.s_huge = 1;
       return;
     }
     int pos = atomicAdd(&S.s_n, 1);
-    st_cg(P.q[sdst] + pos, v);                 // complete copy in global memory (grid resume)
+    st_cg(Q[sdst] + pos, v);                 // complete copy in global memory (grid resume)
     if (pos < kSmallCap) S.sq[sa ^ 1][pos] = v;
     atomicMax(&S.s_maxdeg, dg);
   };
@@ -558,9 +577,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     if (state == S_ROUND && (S.bc.flags & 8)) {   // (TC sweeps skip lifted vertices by h >= n)
       // ------------------------------------------------------------ gap lift (A6)
       const int sqn = S.bc.qn, shc = S.bc.hc;
-      const int gl = ld_cg(&C->gap_pending);
+      const int gl = ld_cg(&GC->gap_pending);
       unsigned long long lifted = 0;
-      for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
+      for (int v = VLO + brank * blockDim.x + threadIdx.x; v < VHI; v += nb * blockDim.x) {
         int hv = ld_cg(P.h + v);
         if (hv > gl && hv < N) {
           st_cg(P.h + v, N);
@@ -570,7 +589,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       }
       unsigned long long t = block_sum_u64(S, lifted);
       if (threadIdx.x == 0 && t) atomicAdd((unsigned long long*)&C->stats[ST_GAPLIFT], t);
-      if (blockIdx.x == 0 && threadIdx.x == 0) ring(ph)->kind = PK_GAP;
+      if (brank == 0 && threadIdx.x == 0) ring(ph)->kind = PK_GAP;
       if (!gsync()) return;
       if (threadIdx.x == 0) { S.bc.qn = sqn; S.bc.hc = shc; S.bc.flags = 0; }
       __syncthreads();
@@ -578,16 +597,16 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     }
     if (S.bc.flags & 4) {
       // ------------------------------------------------------------ small-frontier mode
-      if (blockIdx.x == 0) {
+      if (brank == 0) {
         int qa = S.bc.qn;
-        const int* gsrc = (state == S_BFS) ? P.q[fb] : P.q[cur];
+        const int* gsrc = (state == S_BFS) ? Q[fb] : Q[cur];
         for (int i = threadIdx.x; i < qa; i += blockDim.x) S.sq[0][i] = ld_cg(gsrc + i);
         // thread 0 keeps the GR-policy state and counters in registers while CTA 0 runs alone
         unsigned long long g_work = 0, g_after = 0, g_grtime = 0;
         long long c_rounds = 0, c_avq = 0, c_levels = 0, c_phases = 0;
         if (threadIdx.x == 0) {
-          C->small_hn = 0; C->small_hc = 0; C->stats[ST_SMALL_ENTRIES]++;
-          g_work = C->pol.work_since_gr; g_after = C->pol.t_after_gr; g_grtime = C->pol.gr_time;
+          GC->small_hn = 0; GC->small_hc = 0; atomicAdd((unsigned long long*)&C->stats[ST_SMALL_ENTRIES], 1ull);
+          g_work = GC->pol.work_since_gr; g_after = GC->pol.t_after_gr; g_grtime = GC->pol.gr_time;
         }
         sa = 0;
         int code = 0, nn = 0;
@@ -618,10 +637,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
               g_work += S.s_work;
               bool due = (nn == 0 && !S.s_huge) || g_work >= gr_threshold ||
                          (P.gr_gamma > 0.f && (double)(now - g_after) >= (double)P.gr_gamma * (double)g_grtime);
-              if (due) { C->pol.t_gr_start = now; ex = 3; }
+              if (due) { GC->pol.t_gr_start = now; ex = 3; }
               else if (rounds >= P.max_rounds) { C->status = DS_NOTCONVERGED; ex = 4; }
-              else if (P.gap_mode && ld_cg(&C->gap_level) < N) {
-                C->gap_pending = C->gap_level; C->gap_level = N; ex = 6;
+              else if (P.gap_mode && ld_cg(&GC->gap_level) < N) {
+                GC->gap_pending = GC->gap_level; GC->gap_level = N; ex = 6;
               }
               else if (spill) ex = 1;
             }
@@ -638,16 +657,17 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
         else if (code == 3) state = S_GR;
         else if (code == 4 || code == 5) state = S_DONE;
         if (threadIdx.x == 0) {
-          C->pol.work_since_gr = g_work;
-          C->stats[ST_ROUNDS] += c_rounds; C->stats[ST_AVQ] += c_avq;
-          C->stats[ST_BFS_LEVELS] += c_levels; C->stats[ST_SMALL_PHASES] += c_phases;
-          Resume& R = C->res;
-          R.state = state; R.qn = nn; R.hc = C->small_hc; R.cur = cur; R.fb = fb; R.level = level;
+          GC->pol.work_since_gr = g_work;
+          l_rounds += c_rounds; l_levels += c_levels;
+          atomicAdd((unsigned long long*)&C->stats[ST_AVQ], (unsigned long long)c_avq);
+          atomicAdd((unsigned long long*)&C->stats[ST_SMALL_PHASES], (unsigned long long)c_phases);
+          Resume& R = GC->res;
+          R.state = state; R.qn = nn; R.hc = GC->small_hc; R.cur = cur; R.fb = fb; R.level = level;
           R.rounds = rounds;
           R.flags = code == 6 ? 8 : 0;
           __threadfence();
           atomicAdd(&R.epoch, 1u);
-          S.bc.qn = nn; S.bc.hc = C->small_hc; S.bc.flags = code == 6 ? 8 : 0;
+          S.bc.qn = nn; S.bc.hc = GC->small_hc; S.bc.flags = code == 6 ? 8 : 0;
           S.abort = code == 5;
         }
         ++small_epoch;
@@ -658,13 +678,13 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           const unsigned target = small_epoch + 1;
           int ab = 0;
           unsigned ns = 32;
-          while (ld_acquire(&C->res.epoch) != target) {
+          while (ld_acquire(&GC->res.epoch) != target) {
             if (ld_volatile(&C->abort)) { ab = 1; break; }
             if (globaltimer() > deadline) { atomicExch(&C->abort, 1); ab = 1; break; }
             __nanosleep(ns);
             if (ns < 256) ns <<= 1;
           }
-          Resume& R = C->res;
+          Resume& R = GC->res;
           S.bc.qn = ld_cg(&R.qn); S.bc.hc = ld_cg(&R.hc); S.bc.flags = (unsigned)ld_cg(&R.flags);
           S.s_n = ld_cg(&R.state); S.s_maxdeg = ld_cg(&R.cur); S.s_huge = ld_cg(&R.fb); S.s_exit = ld_cg(&R.level);
           S.s_work = (unsigned long long)ld_cg(&R.rounds);
@@ -682,24 +702,24 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     if (state == S_GR) {
       // ------------------------------------------------------------ global relabel
       // reset labels: sinks 0, everything else |V| (= unreached); frontier <- sinks
-      for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
+      for (int v = VLO + brank * blockDim.x + threadIdx.x; v < VHI; v += nb * blockDim.x) {
         st_cg(P.h + v, (ld_term(P.term + v) & kSink) ? 0 : ((ld_term(P.term + v) & kSource) ? N + 1 : N));
         if (P.gap_mode) st_cg(P.hist + v, 0);
       }
-      if (blockIdx.x == 0) {
+      if (brank == 0) {
         QueueOut o = out_for(0);
-        for (int base = w * 32; base < P.k; base += kWarps * 32) {
+        for (int base = w * 32; base < KI; base += kWarps * 32) {
           int i = base + lane;
-          int t = i < P.k ? (int)SNK[i] : 0;
-          int dg = i < P.k ? ops.degree(t) : 0;
-          bool huge = i < P.k && dg > kChunk;
+          int t = i < KI ? (int)SNK[i] : 0;
+          int dg = i < KI ? ops.degree(t) : 0;
+          bool huge = i < KI && dg > kChunk;
           if (huge) huge_append(t, dg, o);
-          warp_append(S, cnt, i < P.k && !huge, t, o, dg);
+          warp_append(S, cnt, i < KI && !huge, t, o, dg);
           unsigned fsum = warp_sum((unsigned)dg);
           if (lane == 0 && fsum) atomicAdd(&ring(ph)->fedges, fsum);
         }
         block_flush_all(S, cnt, o);
-        if (threadIdx.x == 0) { C->stats[ST_GRS]++; ring(ph)->kind = PK_GR_RESET; }
+        if (threadIdx.x == 0) { ++l_grs; ring(ph)->kind = PK_GR_RESET; }
       }
       if (!gsync()) return;
       state = S_BFS;
@@ -716,9 +736,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
         unsigned fedges = 0;   // lane 0: slots of the vertices this warp appended
         if (!(S.bc.flags & 2)) {
           // ---- top-down: frontier vertex w, in-arcs u -> w with c_f > 0
-          const int* qf = P.q[fb];
-          const HugeRec* hqf = P.hq[fb];
-          const int2* hcf = P.hc[fb];
+          const int* qf = Q[fb];
+          const HugeRec* hqf = HQ[fb];
+          const int2* hcf = HC[fb];
           int total = qn + hc;
           for (int tk = gwarp; tk < total; tk += nwarps) {
             int wv, lo, hi;
@@ -757,9 +777,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
         } else {
           // ---- bottom-up: every unlabelled vertex v looks for an out-arc v -> w with
           // c_f > 0 and level(w) = level (early exit per 32-slot group)
-          for (int base = (blockIdx.x * kWarps + w) * 32; base < N; base += nwarps * 32) {
+          for (int base = VLO + gwarp * 32; base < VHI; base += nwarps * 32) {
             int v = base + lane;
-            int hv = v < N ? ld_cg_hint(P.h + v, pl) : -1;
+            int hv = v < VHI ? ld_cg_hint(P.h + v, pl) : -1;
             unsigned todo = __ballot_sync(FULL, hv == N);
             unsigned found_mask = 0;
             while (todo) {
@@ -795,9 +815,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
             warp_append(S, cnt, found, v, o, dg);
           }
           // unlabelled hubs: one warp per 1024-slot chunk, first finder labels (CAS)
-          const int nhs = ld_cg(&C->nhs);
+          const int nhs = ld_cg(&GC->nhs);
           for (int t = gwarp; t < nhs; t += nwarps) {
-            int2 hsk = ld_cg(P.hs + t);
+            int2 hsk = ld_cg(HS + t);
             int vv = hsk.x;
             if (ld_cg_hint(P.h + vv, pl) != N) continue;
             Seg sg = ops.seg(vv);
@@ -829,7 +849,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           if (threadIdx.x == 0 && t) atomicAdd(&ring(ph)->fedges, (unsigned)t);
         }
         block_flush_all(S, cnt, o);
-        if (blockIdx.x == 0 && threadIdx.x == 0) { C->stats[ST_BFS_LEVELS]++; ring(ph)->kind = PK_BFS; }
+        if (brank == 0 && threadIdx.x == 0) { ++l_levels; ring(ph)->kind = PK_BFS; }
       }
       if (!gsync()) return;
       fb ^= 1;
@@ -847,16 +867,16 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           for (int i = threadIdx.x; i < kGapBins; i += blockDim.x) S.gbin[i] = 0;
           __syncthreads();
         }
-        for (int base = blockIdx.x * blockDim.x + w * 32; base < N; base += nb * blockDim.x) {
+        for (int base = VLO + brank * blockDim.x + w * 32; base < VHI; base += nb * blockDim.x) {
           int v = base + lane;
           bool act = false, huge = false;
           int dg = 0;
-          if (P.gap_mode && v < N) {
+          if (P.gap_mode && v < VHI) {
             int hv0 = ld_cg(P.h + v);
             if (hv0 < kGapBins) atomicAdd(&S.gbin[hv0], 1);
             else if (hv0 < N) atomicAdd(P.hist + hv0, 1);
           }
-          if (v < N) {
+          if (v < VHI) {
             long long ev = ld_cg(P.e + v);
             if (ev > 0 && ld_term(P.term + v) == 0) {
               int hv = ld_cg(P.h + v);
@@ -870,14 +890,14 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
               }
             }
           }
-          if (lane == 0) st_cand += min(32, N - base);
+          if (lane == 0) st_cand += min(32, VHI - base);
           if (huge) huge_append(v, dg, o);
           warp_append(S, cnt, act && !huge, v, o, dg);
         }
         block_flush_all(S, cnt, o);
         unsigned long long t = block_sum_u64(S, dropped);
         if (threadIdx.x == 0 && t) atomicAdd((unsigned long long*)&C->excess_total, (unsigned long long)(-(long long)t));
-        if (blockIdx.x == 0 && threadIdx.x == 0) ring(ph)->kind = PK_COMPACT;
+        if (brank == 0 && threadIdx.x == 0) ring(ph)->kind = PK_COMPACT;
         if (P.gap_mode)
           for (int i = threadIdx.x; i < kGapBins && i < N; i += blockDim.x)
             if (S.gbin[i]) atomicAdd(P.hist + i, S.gbin[i]);
@@ -894,12 +914,12 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       // ------------------------------------------------------------ thread-centric sweep
       // Alg. 1 Step 1: every thread tests its vertices for activity and scans
       // their residual arcs serially (NEXT #1: the paper's comparison baseline)
-      if (blockIdx.x == 0 && threadIdx.x == 0) { C->stats[ST_ROUNDS]++; ring(ph)->kind = PK_ROUND; }
+      if (brank == 0 && threadIdx.x == 0) { ++l_rounds; ring(ph)->kind = PK_ROUND; }
       unsigned long long active = 0;
       tc_work = 0;
       unsigned long long tt0; long long ta0, tp0, tr0c; int tn0;
       trace_begin(tt0, ta0, tp0, tr0c, tn0);
-      for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
+      for (int v = VLO + brank * blockDim.x + threadIdx.x; v < VHI; v += nb * blockDim.x) {
         if (ld_cg(P.e + v) > 0 && ld_term(P.term + v) == 0 && ld_cg(P.h + v) < N) {
           ++active;
           small_round_vertex(v, true);
@@ -917,7 +937,7 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       if (!gsync()) return;
       ++rounds;
       if (rounds >= P.max_rounds) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) { C->status = DS_NOTCONVERGED; }
+        if (brank == 0 && threadIdx.x == 0) { C->status = DS_NOTCONVERGED; }
         state = S_DONE;
         continue;
       }
@@ -927,16 +947,16 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
 
     // -------------------------------------------------------------- one push/relabel round
     {
-      const unsigned long long tr0 = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer() : 0;
+      const unsigned long long tr0 = (brank == 0 && threadIdx.x == 0) ? globaltimer() : 0;
       const int qn = S.bc.qn, hc = S.bc.hc;
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        C->stats[ST_ROUNDS]++;
+      if (brank == 0 && threadIdx.x == 0) {
+        ++l_rounds;
         ring(ph)->kind = PK_ROUND;
       }
       QueueOut o = out_for(cur ^ 1);
-      const int* qc = P.q[cur];
-      HugeRec* hqc = P.hq[cur];
-      const int2* hcc = P.hc[cur];
+      const int* qc = Q[cur];
+      HugeRec* hqc = HQ[cur];
+      const int2* hcc = HC[cur];
       unsigned long long work = 0;
       const int total = qn + hc;
       unsigned long long tt0; long long ta0, tp0, tr0c; int tn0;
@@ -1097,16 +1117,16 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
       }
       trace_end(tt0, ta0, tp0, tr0c, tn0);
       ++trace_round;
-      const unsigned long long tf0 = (blockIdx.x == 0 && threadIdx.x == 0) ? globaltimer() : 0;
+      const unsigned long long tf0 = (brank == 0 && threadIdx.x == 0) ? globaltimer() : 0;
       block_flush_all(S, cnt, o);
       unsigned long long t = block_sum_u64(S, work);
       if (threadIdx.x == 0 && t) atomicAdd(&ring(ph)->work, (unsigned)(t < 0x7fffffffull ? t : 0x7fffffffull));
-      if (blockIdx.x == 0 && threadIdx.x == 0) { t_flush += globaltimer() - tf0; t_round += tf0 - tr0; }
+      if (brank == 0 && threadIdx.x == 0) { t_flush += globaltimer() - tf0; t_round += tf0 - tr0; }
       if (!gsync()) return;
       cur ^= 1;
       ++rounds;
       if (rounds >= P.max_rounds) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) { C->status = DS_NOTCONVERGED; }
+        if (brank == 0 && threadIdx.x == 0) { C->status = DS_NOTCONVERGED; }
         state = S_DONE;
         continue;
       }
@@ -1119,12 +1139,12 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
   // terminal roles and run the same loop toward the sources, which returns every
   // stranded unit of excess to s through the residual arcs (a true flow).
   if (phase == 1 && P.phase2 && converged) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < N; v += nb * blockDim.x) {
+    for (int v = VLO + brank * blockDim.x + threadIdx.x; v < VHI; v += nb * blockDim.x) {
       st_cg(P.h1 + v, ld_cg(P.h + v));
       uint8_t tv = P.term[v];
       P.term[v] = (uint8_t)(((tv & kSource) ? kSink : 0) | ((tv & kSink) ? kSource : 0));
     }
-    SNK = P.src;
+    SNK = P.src + I0;
     phase = 2;
     converged = false;
     state = S_GR;
@@ -1135,6 +1155,11 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
   }
 
   // ---------------------------------------------------------------- statistics
+  if (brank == 0 && threadIdx.x == 0) {   // rounds / GRs / levels: max over the groups
+    atomicMax((unsigned long long*)&C->stats[ST_ROUNDS], (unsigned long long)l_rounds);
+    atomicMax((unsigned long long*)&C->stats[ST_GRS], (unsigned long long)l_grs);
+    atomicMax((unsigned long long*)&C->stats[ST_BFS_LEVELS], (unsigned long long)l_levels);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     C->stats[ST_COUNT - 3] = (long long)t_sync;
     C->stats[ST_COUNT - 2] = (long long)t_flush;

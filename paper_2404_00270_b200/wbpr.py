@@ -45,7 +45,7 @@ class Options(ctypes.Structure):
                 ("max_rounds", ctypes.c_int64), ("grid_blocks", ctypes.c_int32), ("timeout_ms", ctypes.c_int32),
                 ("push_mode", ctypes.c_int32), ("gr_gamma", ctypes.c_float), ("l2_persist", ctypes.c_int32),
                 ("bfs_mode", ctypes.c_int32), ("small_mode", ctypes.c_int32), ("schedule", ctypes.c_int32),
-                ("phase2", ctypes.c_int32), ("trace_rounds", ctypes.c_int32)]
+                ("phase2", ctypes.c_int32), ("trace_rounds", ctypes.c_int32), ("batch_groups", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -117,7 +117,8 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
             timeout_ms: int = 0, push_mode: Optional[int] = None, gr_gamma: Optional[float] = None,
             l2_persist: Optional[int] = None, bfs_mode: Optional[int] = None,
             small_mode: Optional[int] = None, schedule: Optional[str] = None,
-            phase2: Optional[int] = None, trace_rounds: Optional[int] = None) -> Options:
+            phase2: Optional[int] = None, trace_rounds: Optional[int] = None,
+            batch_groups: Optional[int] = None) -> Options:
     o = Options()
     _check(load().wbpr_default_options(ctypes.byref(o)))
     o.layout = _LAYOUTS[layout]
@@ -144,6 +145,8 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
         o.phase2 = phase2
     if trace_rounds is not None:
         o.trace_rounds = trace_rounds
+    if batch_groups is not None:
+        o.batch_groups = batch_groups
     return o
 
 

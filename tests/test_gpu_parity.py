@@ -212,14 +212,20 @@ def test_bipartite_spec_examples(golden):
 
 # ------------------------------------------------------------------ batch (A10)
 @pytest.mark.parametrize("layout", LAYOUTS)
-def test_batch_union(layout):
+@pytest.mark.parametrize("groups", [0, 2, 5, 11])
+@pytest.mark.parametrize("phase2", [0, 1])
+def test_batch_union(layout, groups, phase2):
+    # groups 0 / 1: one solver for the union (default); 2 / 5: contiguous instance ranges per
+    # solver group
     import torch
     import paper_2404_00270_b200 as W
     parts = [synth.rmat(11, 16, 100 + i, "paper" if i % 2 else "hub20") for i in range(6)]
     parts += [synth.random_graph(500, 3000, i, 0, 499) for i in range(3)]
+    parts += [synth.grid(20, 15, True, 4), synth.tiny_random(8, 20, 5, 2, self_loops=False, s=0, t=7)]
     B = synth.disjoint_union(parts)
     ro, col, cap = to_dev(B.union)
-    flows, cuts, bm, st = W.maxflow_batch(ro, col, cap, B.vbase, B.s, B.t, layout=layout)
+    flows, cuts, bm, st = W.maxflow_batch(ro, col, cap, B.vbase, B.s, B.t, layout=layout, batch_groups=groups,
+                                          phase2=phase2)
     mask = bits_to_mask(bm.cpu().numpy().view(np.uint32), B.union.n)
     for i, g in enumerate(parts):
         ref = oracle.maxflow_graph(g, phase2=False)

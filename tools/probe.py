@@ -39,6 +39,7 @@ ap.add_argument("--bfs", type=int, default=1)
 ap.add_argument("--small", type=int, default=1)
 ap.add_argument("--gap", type=int, default=0)
 ap.add_argument("--schedule", default="vc")
+ap.add_argument("--groups", type=int, default=0)
 ap.add_argument("--oracle", action="store_true")
 a = ap.parse_args()
 for name in a.cfgs:
@@ -55,7 +56,7 @@ for name in a.cfgs:
                                                   gr_beta=a.beta, timeout_ms=100000, grid_blocks=a.blocks,
                                                   push_mode=a.mode, gr_gamma=a.gamma, l2_persist=a.persist,
                                                   bfs_mode=a.bfs, small_mode=a.small, gap_mode=a.gap,
-                                                  schedule=a.schedule)
+                                                  schedule=a.schedule, batch_groups=a.groups)
             print(json.dumps(dict(cfg=name, rep=rep, gen_s=round(gen, 2), **st)), flush=True)
         continue
     if name == "c4":
