@@ -52,9 +52,11 @@ __global__ void k_rows(const int64_t* __restrict__ ro, int64_t n, int64_t m, int
 constexpr int kEdgesPerThread = 8;
 
 // Validation + in-degree histogram of the non-self-loop half-arcs.
+// Validation + in-degree histogram, fused with the 64-bit row keys (col << 32 | cap,
+// self-loops = all ones) and the per-row "not column-sorted" flags the construction needs.
 __global__ void k_edges(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
                         const int32_t* __restrict__ cap, int64_t n, int64_t m, int* indeg, Ctrl* ctrl,
-                        int count_in, const int64_t* __restrict__ vbase, int k) {
+                        int count_in, const int64_t* __restrict__ vbase, int k, uint64_t* keys, uint8_t* need) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t i0 = t * kEdgesPerThread;
   int loops = 0;
@@ -76,6 +78,13 @@ __global__ void k_edges(const int64_t* __restrict__ ro, const int32_t* __restric
         lo = __ldg(vbase + a); hi = __ldg(vbase + a + 1);
       }
       int v = col[i], c = cap[i];
+      uint64_t key = (v == u) ? kSent : (((uint64_t)(uint32_t)v << 32) | (uint32_t)c);
+      keys[i] = key;
+      if (i > __ldg(ro + u)) {
+        int pv = col[i - 1];
+        uint64_t pk = (pv == u) ? kSent : (((uint64_t)(uint32_t)pv << 32) | (uint32_t)cap[i - 1]);
+        if (key < pk) need[u] = 1;
+      }
       if (v < lo || v >= hi || c < 0) {
         atomicMin((unsigned long long*)&ctrl->bad_edge, (unsigned long long)i);
         continue;
@@ -197,9 +206,10 @@ __global__ void k_colcopy(const int2* __restrict__ arc, const Ctrl* ctrl, int* c
 }
 
 // mate[p] = position of the owner u inside seg(col[p]) — binary search on the
-// sorted segment, done once per arc PAIR: the slot with the smaller
-// endpoint searches and writes both directions.  8 consecutive slots per thread
-// share one owner search.
+// sorted segment, done once per arc PAIR: the endpoint with the larger
+// segment searches the smaller one (ties: the smaller id searches) and writes both
+// directions, so hub pairs cost log2(deg(leaf)) probes, not log2(deg(hub)).
+// 8 consecutive slots per thread share one owner search.
 __global__ void k_mate(const int* __restrict__ off, const int* __restrict__ colv, int n, const Ctrl* ctrl_c,
                        int* mate, Ctrl* ctrl) {
   const int M = ctrl_c->M;
@@ -208,11 +218,13 @@ __global__ void k_mate(const int* __restrict__ off, const int* __restrict__ colv
   if (p0 >= M) return;
   int u = row_of32(off, n, (int)p0);
   int p1 = (int)(p0 + kEdgesPerThread < (int64_t)M ? p0 + kEdgesPerThread : (int64_t)M);
+  int ub = __ldg(off + u), ue = __ldg(off + u + 1);
   for (int p = (int)p0; p < p1; ++p) {
-    while (__ldg(off + u + 1) <= p) ++u;
+    while (ue <= p) { ++u; ub = ue; ue = __ldg(off + u + 1); }
     int v = __ldg(colv + p);
-    if (v < u) continue;          // the pair is handled from its smaller endpoint
     int lo = __ldg(off + v), end = __ldg(off + v + 1), hi = end;
+    int du = ue - ub, dv = end - lo;
+    if (dv > du || (dv == du && v < u)) continue;   // the pair is handled from v
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
       if (__ldg(colv + mid) < u) lo = mid + 1; else hi = mid;
@@ -275,9 +287,12 @@ void build_validate(const BuildArgs& a, cudaStream_t st) {
   if (a.layout == 0) cudaMemsetAsync(a.deg, 0, sizeof(int) * a.n, st);
   { k_rows<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.ro, a.n, a.m, a.deg, a.ctrl, a.layout != 0); note_launch(); }
   int64_t threads = (a.m + kEdgesPerThread - 1) / kEdgesPerThread;
+  // row keys go to region B (BCSR merge build) / region A (RCSR forward sort)
+  cudaMemsetAsync(a.need, 0, a.n, st);
   if (a.m > 0)
     { k_edges<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, a.n, a.m, a.deg, a.ctrl,
-                                                   a.layout == 0 ? 1 : 0, a.vbase, a.k); note_launch(); }
+                                                   a.layout == 0 ? 1 : 0, a.vbase, a.k,
+                                                   a.layout == 0 ? a.tmp : a.keys, a.need); note_launch(); }
   { k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl); note_launch(); }
 }
 
@@ -319,8 +334,7 @@ void build_rcsr_forward(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
   const int64_t n = a.n, m = a.m;
   { k_ro_to_i32<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.ro, n, a.soff); note_launch(); }
-  // rows already column-sorted in the input are not sorted again
-  outkeys_need(a, a.keys, st);
+  // rows already column-sorted in the input are not sorted again (keys + flags from k_edges)
   segmented_sort_filtered(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.need, a.ctrl, a.arc, a.arc + a.H / 2, a.q0,
                           a.num_sms, st);
   int* flags = (int*)a.tmp;

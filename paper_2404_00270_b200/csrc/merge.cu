@@ -300,11 +300,10 @@ void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
   uint64_t* otmp = reinterpret_cast<uint64_t*>(a.arc);        // region C [0, 8m)
   int2* items = a.arc + m;                                    // region C [8m, 12m)
   int2* items_med = a.arc + m + m / 2 + 1;                    // region C [12m, 16m)
-  cudaMemsetAsync(a.need, 0, n, st);
+  // out-keys and their sortedness flags were written by the validation pass (k_edges)
   cudaMemsetAsync(a.cursor, 0, sizeof(int) * n, st);
   int64_t threads = (m + 7) / 8;
   if (m > 0) {
-    { k_outkeys<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, outk, a.need); note_launch(); }
     { k_inscatter<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(a.ro, a.col, n, m, a.rsoff, a.cursor, ink); note_launch(); }
   }
   segmented_sort_filtered(outk, otmp, a.soff, (int)n, a.maxlen_out, a.need, a.ctrl, items, items_med, a.q0,
