@@ -140,6 +140,11 @@ typedef struct wbpr_stats {
   int64_t kernel_launches;   /* kernels this call launched (all of them this library's own) */
   int64_t t_barrier_ns, t_flush_ns, t_round_ns; /* CTA 0 time in grid barriers / queue flushes /
                                                    round task loops (globaltimer)             */
+  int64_t phase_ns[9];       /* solve time by phase kind, barrier release to release
+                                (globaltimer): 0 init, 1 push/relabel rounds, 2 GR label
+                                reset, 3 top-down BFS levels, 4 compactions, 5 preflow,
+                                6 gap lifts, 7 bottom-up BFS levels, 8 small-frontier spans */
+  int64_t phase_count[9];    /* phases per kind (small-frontier: phases run in CTA mode)  */
 } wbpr_stats;
 
 /* Fill *opt with the defaults above. */

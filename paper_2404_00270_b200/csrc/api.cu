@@ -124,7 +124,10 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
   a.q1 = at<int>(W.base, L.q1);
   a.mtasks = at<int2>(W.base, L.hc0);
   a.mheads = at<int>(W.base, L.hc1);
-  a.colv = at<int>(W.base, L.regA + 4 * (size_t)L.m);
+  a.ine = at<int>(W.base, L.regA + 4 * (size_t)L.m);
+  a.src = at<int>(W.base, L.regA + 8 * (size_t)L.m);
+  a.pend = at<int>(W.base, L.regA + 8 * (size_t)L.m);
+  a.outslot = at<int>(W.base, L.regD);
 
   build_validate(a, st);
   CK(cudaGetLastError());
@@ -487,6 +490,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
     stats->t_barrier_ns = c.stats[ST_COUNT - 3];
     stats->t_flush_ns = c.stats[ST_COUNT - 2];
     stats->t_round_ns = c.stats[ST_COUNT - 1];
+    for (int i = 0; i < kPhBuckets; ++i) { stats->phase_ns[i] = c.phase_ns[i]; stats->phase_count[i] = c.phase_cnt[i]; }
   }
   if (c.status == DS_NOTCONVERGED) return fail(WBPR_ENOTCONVERGED, "round cap exceeded");
   if (c.abort) return fail(WBPR_ENOTCONVERGED, "device watchdog timeout");

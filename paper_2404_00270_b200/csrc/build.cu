@@ -51,50 +51,63 @@ __global__ void k_rows(const int64_t* __restrict__ ro, int64_t n, int64_t m, int
 
 constexpr int kEdgesPerThread = 8;
 
-// Validation + in-degree histogram of the non-self-loop half-arcs.
 // Validation + in-degree histogram, fused with the 64-bit row keys (col << 32 | cap,
 // self-loops = all ones) and the per-row "not column-sorted" flags the construction needs.
-__global__ void k_edges(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
-                        const int32_t* __restrict__ cap, int64_t n, int64_t m, int* indeg, Ctrl* ctrl,
-                        int count_in, const int64_t* __restrict__ vbase, int k, uint64_t* keys, uint8_t* need) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t i0 = t * kEdgesPerThread;
+// One warp per kEdgeChunk consecutive edges as rows of 32 (coalesced loads and key
+// stores; owners by warp_owner; the previous key of lane 0 is carried across rows).
+constexpr int kEdgeRows = 8;
+constexpr int kEdgeChunk = 32 * kEdgeRows * 8;
+__global__ void __launch_bounds__(256) k_edges(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                                               const int32_t* __restrict__ cap, int64_t n, int64_t m, int* indeg,
+                                               Ctrl* ctrl, int count_in, const int64_t* __restrict__ vbase, int k,
+                                               uint64_t* keys, uint8_t* need, int* src) {
+  const int lane = lane_id();
+  const int64_t E0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kEdgeChunk;
+  if (E0 >= m) return;
+  const int64_t E1 = E0 + kEdgeChunk < m ? E0 + kEdgeChunk : m;
+  int ucur = (int)row_of(ro, n, E0);
+  // carry: owner and key of edge eb - 1 (the edge before lane 0's)
+  int cu = -1;
+  uint64_t ck = 0;
+  if (E0 > 0) {
+    cu = (int)row_of(ro, n, E0 - 1);
+    const int pv = __ldg(col + E0 - 1);
+    ck = (pv == cu) ? kSent : (((uint64_t)(uint32_t)pv << 32) | (uint32_t)__ldg(cap + E0 - 1));
+  }
+  int64_t ilo = 0, ihi = k > 1 ? 0 : n;   // instance [ilo, ihi) of the lane's current owner (A10)
   int loops = 0;
-  if (i0 < m) {
-    int64_t u = row_of(ro, n, i0);
-    // batch (A10): the instance [lo, hi) owning row u; edges must stay inside it
-    int64_t lo = 0, hi = n;
-    if (k > 1) {
+  for (int64_t eb = E0; eb < E1; eb += 32) {
+    const int64_t i = eb + lane;
+    const bool ok = i < E1;
+    const int u = warp_owner(ro, (int)n, ucur, ok ? i : E1 - 1);
+    ucur = __shfl_sync(FULL, u, 31);
+    const int v = ok ? __ldg(col + i) : 0;
+    const int c = ok ? __ldg(cap + i) : 0;
+    const uint64_t key = (v == u) ? kSent : (((uint64_t)(uint32_t)v << 32) | (uint32_t)c);
+    const int pu0 = __shfl_up_sync(FULL, u, 1);
+    const uint64_t pk0 = __shfl_up_sync(FULL, key, 1);
+    const int pu = lane == 0 ? cu : pu0;
+    const uint64_t pk = lane == 0 ? ck : pk0;
+    cu = __shfl_sync(FULL, u, 31);
+    ck = __shfl_sync(FULL, key, 31);
+    if (!ok) continue;
+    keys[i] = key;
+    if (src) src[i] = u;
+    if (pu == u && key < pk) need[u] = 1;
+    if (k > 1 && (u < ilo || u >= ihi)) {
       int a = 0, b = k;
       while (b - a > 1) { int mid = (a + b) >> 1; if (__ldg(vbase + mid) <= u) a = mid; else b = mid; }
-      lo = __ldg(vbase + a); hi = __ldg(vbase + a + 1);
+      ilo = __ldg(vbase + a); ihi = __ldg(vbase + a + 1);
     }
-    int64_t i1 = i0 + kEdgesPerThread < m ? i0 + kEdgesPerThread : m;
-    for (int64_t i = i0; i < i1; ++i) {
-      while (__ldg(ro + u + 1) <= i) ++u;
-      while (u >= hi) {
-        int a = 0, b = k;
-        while (b - a > 1) { int mid = (a + b) >> 1; if (__ldg(vbase + mid) <= u) a = mid; else b = mid; }
-        lo = __ldg(vbase + a); hi = __ldg(vbase + a + 1);
-      }
-      int v = col[i], c = cap[i];
-      uint64_t key = (v == u) ? kSent : (((uint64_t)(uint32_t)v << 32) | (uint32_t)c);
-      keys[i] = key;
-      if (i > __ldg(ro + u)) {
-        int pv = col[i - 1];
-        uint64_t pk = (pv == u) ? kSent : (((uint64_t)(uint32_t)pv << 32) | (uint32_t)cap[i - 1]);
-        if (key < pk) need[u] = 1;
-      }
-      if (v < lo || v >= hi || c < 0) {
-        atomicMin((unsigned long long*)&ctrl->bad_edge, (unsigned long long)i);
-        continue;
-      }
-      if (v == u) { ++loops; continue; }
-      if (count_in) atomicAdd(indeg + v, 1);
+    if (v < ilo || v >= ihi || c < 0) {
+      atomicMin((unsigned long long*)&ctrl->bad_edge, (unsigned long long)i);
+      continue;
     }
+    if (v == u) { ++loops; continue; }
+    if (count_in) atomicAdd(indeg + v, 1);
   }
   loops = warp_sum(loops);
-  if (lane_id() == 0 && loops) atomicAdd(&ctrl->selfloops, loops);
+  if (lane == 0 && loops) atomicAdd(&ctrl->selfloops, loops);
 }
 
 __global__ void k_add(int* a, const int* __restrict__ b, int64_t n) {
@@ -205,34 +218,29 @@ __global__ void k_colcopy(const int2* __restrict__ arc, const Ctrl* ctrl, int* c
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < M; p += gridDim.x * blockDim.x) colv[p] = arc[p].x;
 }
 
-// mate[p] = position of the owner u inside seg(col[p]) — binary search on the
-// sorted segment, done once per arc PAIR: the endpoint with the larger
-// segment searches the smaller one (ties: the smaller id searches) and writes both
-// directions, so hub pairs cost log2(deg(leaf)) probes, not log2(deg(hub)).
-// 8 consecutive slots per thread share one owner search.
-__global__ void k_mate(const int* __restrict__ off, const int* __restrict__ colv, int n, const Ctrl* ctrl_c,
-                       int* mate, Ctrl* ctrl) {
+// mate[] from the edge identities carried through the construction (merge.cu): every
+// slot q that received an in-half-arc of input edge e = (u -> x) pairs with the slot
+// outslot[e] of e's out-half-arc in seg(u) — the paper's backward-arc binary search
+// replaced by one lookup per pair.  Pairs with arcs in both directions are
+// written from both sides (same values); every slot is written by itself or its partner.
+constexpr int kMatePerThread = 4;
+__global__ void __launch_bounds__(256) k_mate(const int* __restrict__ pend, const int* __restrict__ outslot,
+                                              const Ctrl* ctrl_c, int* mate) {
   const int M = ctrl_c->M;
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t p0 = t * kEdgesPerThread;
-  if (p0 >= M) return;
-  int u = row_of32(off, n, (int)p0);
-  int p1 = (int)(p0 + kEdgesPerThread < (int64_t)M ? p0 + kEdgesPerThread : (int64_t)M);
-  int ub = __ldg(off + u), ue = __ldg(off + u + 1);
-  for (int p = (int)p0; p < p1; ++p) {
-    while (ue <= p) { ++u; ub = ue; ue = __ldg(off + u + 1); }
-    int v = __ldg(colv + p);
-    int lo = __ldg(off + v), end = __ldg(off + v + 1), hi = end;
-    int du = ue - ub, dv = end - lo;
-    if (dv > du || (dv == du && v < u)) continue;   // the pair is handled from v
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (__ldg(colv + mid) < u) lo = mid + 1; else hi = mid;
-    }
-    if (lo >= end || __ldg(colv + lo) != u) { atomicExch(&ctrl->overflow, 2); continue; }
-    mate[p] = lo;
-    mate[lo] = p;
+  const long long base = (long long)blockIdx.x * blockDim.x * kMatePerThread + threadIdx.x;
+  int e[kMatePerThread], q[kMatePerThread];
+#pragma unroll
+  for (int r = 0; r < kMatePerThread; ++r) {
+    const long long qq = base + (long long)r * blockDim.x;
+    q[r] = qq < M ? (int)qq : -1;
+    e[r] = q[r] >= 0 ? __ldg(pend + q[r]) : -1;
   }
+  int p[kMatePerThread];
+#pragma unroll
+  for (int r = 0; r < kMatePerThread; ++r) p[r] = e[r] >= 0 ? __ldg(outslot + e[r]) : -1;
+#pragma unroll
+  for (int r = 0; r < kMatePerThread; ++r)
+    if (p[r] >= 0) { mate[q[r]] = p[r]; mate[p[r]] = q[r]; }
 }
 
 // RCSR reverse in-degree over forward arcs
@@ -286,13 +294,14 @@ void build_validate(const BuildArgs& a, cudaStream_t st) {
   // BCSR: deg[] = in-degrees (out-rows come straight from the input); RCSR: deg[] = out-degrees
   if (a.layout == 0) cudaMemsetAsync(a.deg, 0, sizeof(int) * a.n, st);
   { k_rows<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.ro, a.n, a.m, a.deg, a.ctrl, a.layout != 0); note_launch(); }
-  int64_t threads = (a.m + kEdgesPerThread - 1) / kEdgesPerThread;
+  int64_t threads = (a.m + kEdgeChunk - 1) / kEdgeChunk * 32;
   // row keys go to region B (BCSR merge build) / region A (RCSR forward sort)
   cudaMemsetAsync(a.need, 0, a.n, st);
   if (a.m > 0)
     { k_edges<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, a.n, a.m, a.deg, a.ctrl,
                                                    a.layout == 0 ? 1 : 0, a.vbase, a.k,
-                                                   a.layout == 0 ? a.tmp : a.keys, a.need); note_launch(); }
+                                                   a.layout == 0 ? a.tmp : a.keys, a.need,
+                                                   a.layout == 0 ? a.src : nullptr); note_launch(); }
   { k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl); note_launch(); }
 }
 
@@ -321,9 +330,9 @@ void build_bcsr(const BuildArgs& a, cudaStream_t st) {
 
 void build_bcsr_mate(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
-  // M is on the device (ctrl->M); H bounds it.  colv (dense columns) was written by the merge.
-  int64_t threads = (a.H + kEdgesPerThread - 1) / kEdgesPerThread;
-  if (a.H > 0) { k_mate<<<grid_exact(threads, T), T, 0, st>>>(a.off, a.colv, (int)a.n, a.ctrl, a.mate, a.ctrl); note_launch(); }
+  // M is on the device (ctrl->M); H bounds it.  pend / outslot were written by the merge.
+  const int64_t per_block = (int64_t)T * kMatePerThread;
+  if (a.H > 0) { k_mate<<<(unsigned)((a.H + per_block - 1) / per_block), T, 0, st>>>(a.pend, a.outslot, a.ctrl, a.mate); note_launch(); }
 }
 
 void k_ro_to_i32_ext(const int64_t* ro, int64_t n, int* out, int num_sms, cudaStream_t st) {

@@ -7,6 +7,7 @@
 //  * Immutable arrays (offsets, columns in a separate array, mate, terminal flags)
 //    go through the read-only path (ld.global.nc).
 #pragma once
+#include <climits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -69,6 +70,34 @@ template <typename T> WBPR_DEV T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
+}
+
+// Owner row of position p in a CSR-like offset array, for a warp walking a row of 32
+// consecutive positions: `base` (warp-uniform) is the owner of the row's first position,
+// i.e. off[base] <= first < off[base + 1].  Each lane returns the u with
+// off[u] <= p < off[u + 1] (p < off[n]); one coalesced load of 32 offsets plus a 5-step
+// shuffle search per 32 vertex boundaries crossed (instead of a log2(n)-deep binary
+// search per thread).  All lanes must call.
+template <typename T>
+WBPR_DEV int warp_owner(const T* __restrict__ off, int n, int base, long long p) {
+  const int lane = threadIdx.x & 31;
+  int owner = -1;
+  while (true) {
+    const int k = base + 1 + lane;
+    const long long wv = k <= n ? (long long)__ldg(off + k) : LLONG_MAX;
+    const long long w31 = __shfl_sync(FULL, wv, 31);
+    int c = 0;   // number of window entries <= p (entries are non-decreasing)
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const long long v = __shfl_sync(FULL, wv, c + s - 1);
+      if (v <= p) c += s;
+    }
+    if (c == 31 && w31 <= p) c = 32;
+    if (owner < 0 && c < 32) owner = base + c;
+    if (!__ballot_sync(FULL, owner < 0)) break;
+    base += 32;
+  }
+  return owner;
 }
 
 // ----------------------------------------------------------------- block reductions

@@ -42,6 +42,10 @@ struct __align__(16) Bcast {
 };
 
 enum PhaseKind { PK_NONE = 0, PK_ROUND = 1, PK_GR_RESET = 2, PK_BFS = 3, PK_COMPACT = 4, PK_PREFLOW = 5, PK_GAP = 6 };
+// phase-time buckets (Ctrl::phase_ns / phase_cnt): the PhaseKinds, plus
+constexpr int kPhBfsUp = 7;     // bottom-up BFS levels (PK_BFS counts the top-down ones)
+constexpr int kPhSmall = 8;     // small-frontier CTA-mode spans (CTA 0 alone)
+constexpr int kPhBuckets = 9;
 
 // Global-relabel policy state, written only by the last CTA to arrive at a barrier.
 struct GrPolicy {
@@ -51,8 +55,9 @@ struct GrPolicy {
   unsigned long long gr_time;
   unsigned long long bfs_seen_edges;   // slots of the vertices labelled so far in this GR
   unsigned long long prev_reached;     // slots labelled by the previous GR (0 = none yet)
+  unsigned long long t_release;        // globaltimer at the last barrier release (phase timing)
   int bfs_bottom_up;                   // direction of the current BFS level
-  int pad;
+  int bfs_bottom_up_prev;              // direction of the BFS level now running (phase timing)
 };
 
 // Huge-vertex record for one round: chunk tasks fold their partial minima into
@@ -131,6 +136,8 @@ struct Ctrl {
   int mlist_w, mlist_c;   // build: vertices merged by a warp / by a CTA
   int maxlen_out;         // build: longest input row
   int pad0[1];
+  long long phase_ns[kPhBuckets];    // solve: barrier-release-to-release time per phase kind
+  long long phase_cnt[kPhBuckets];
 };
 
 // Per-warp workload trace record (NEXT #3): one per warp per traced round.
@@ -152,6 +159,7 @@ struct Layout {
   size_t q0, q1, hq0, hq1, hc0, hc1, hist, hs;
   size_t scan_part;
   size_t regA, regB, regC;                 // build / residual regions
+  size_t regD;                             // BCSR build: slot of every out-half-arc (4m B)
   size_t trace;                            // per-warp trace records
   size_t gdesc, gctrl;                     // solver groups
   size_t bcap0;                            // offset inside regB of cap0
@@ -185,6 +193,7 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout, int32
   L.regB = take(8 * H + 1024);
   L.bcap0 = align_up(4 * H + 260);
   L.regC = take(8 * H + 8);
+  L.regD = take(layout == 0 ? 4 * m + 8 : 8);
   L.trace = take(sizeof(TraceRec) * (size_t)kTraceWarps * (size_t)(trace_rounds > 0 ? trace_rounds : 0) + 32);
   L.gdesc = take(sizeof(GroupDesc) * kMaxGroups);
   L.gctrl = take(sizeof(GroupCtrl) * kMaxGroups);

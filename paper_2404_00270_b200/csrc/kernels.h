@@ -47,7 +47,10 @@ struct BuildArgs {
   int maxlen;
   const int64_t* vbase;  // batch instance ranges (device), k entries + 1
   int k;
-  int* colv;             // dense copy of the merged columns (region A after the merge)
+  int* src;              // BCSR build: owner row of every input edge (region A + 8m; dead after the in-list resolve)
+  int* ine;              // BCSR build: input-edge index of every in-list entry (region A + 4m)
+  int* pend;             // BCSR build: per slot, an in-half-arc's edge index or -1 (region A + 8m)
+  int* outslot;          // BCSR build: per out-half-arc (sorted row position), its merged slot (region D)
   int* rsoff;            // BCSR merge build: in-list offsets
   uint8_t* need;         // BCSR merge build: per-row "not sorted" flags
   int* q1;
@@ -69,6 +72,7 @@ void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st)
 int solve_max_blocks_per_sm(int layout, int threads);
 cudaError_t launch_solve(const SolveParams& p, int blocks, int threads, cudaStream_t st);
 constexpr int kSolveThreads = 512;
+constexpr int kSolveMinBlocks = 2;   // default register budget of k_solve (see solve.cu)
 
 // extract.cu
 void extract_results(const SolveParams& p, const int64_t* ro, const int32_t* col, const int32_t* cap,

@@ -57,20 +57,51 @@ __global__ void k_outkeys(const int64_t* __restrict__ ro, const int32_t* __restr
   }
 }
 
-// in-list scatter: edge (u -> v), u != v, lands in v's list as the 32-bit id u.
-__global__ void k_inscatter(const int64_t* __restrict__ ro, const int32_t* __restrict__ col, int64_t n, int64_t m,
-                            const int* __restrict__ rsoff, int* cursor, uint32_t* inkeys) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t i0 = t * 8;
-  if (i0 >= m) return;
-  int u = row_of64(ro, n, i0);
-  int64_t i1 = i0 + 8 < m ? i0 + 8 : m;
-  for (int64_t i = i0; i < i1; ++i) {
-    while (__ldg(ro + u + 1) <= i) ++u;
-    int v = col[i];
-    if (v == u) continue;
-    int q = rsoff[v] + atomicAdd(cursor + v, 1);
-    inkeys[q] = (uint32_t)u;
+// in-list scatter: the out-half-arc at sorted row position e (edge u -> v, u != v)
+// lands in v's in-list as the 32-bit edge index e (sorting the in-list by e orders it by
+// the source u, since rows are stored in vertex order); k_in_resolve then turns e into
+// u and keeps e beside it, so the merge can pair both half-arcs of the edge (mate[]).
+// One warp per kScatChunk consecutive edges as rows of 32 (coalesced loads); the
+// kScatRows cursor atomics of a lane are issued back to back.
+constexpr int kScatRows = 8;
+constexpr int kScatChunk = 32 * kScatRows * 8;
+__global__ void __launch_bounds__(256) k_inscatter(const uint64_t* __restrict__ outk, int64_t m,
+                                                   const int* __restrict__ rsoff, int* cursor, uint32_t* inkeys) {
+  const int lane = lane_id();
+  const int64_t E0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kScatChunk;
+  if (E0 >= m) return;
+  const int64_t E1 = E0 + kScatChunk < m ? E0 + kScatChunk : m;
+  for (int64_t eb = E0; eb < E1; eb += 32 * kScatRows) {
+    uint64_t k[kScatRows];
+#pragma unroll
+    for (int r = 0; r < kScatRows; ++r) {
+      const int64_t i = eb + r * 32 + lane;
+      k[r] = i < E1 ? __ldg(outk + i) : kSentKey;
+    }
+    int q[kScatRows];
+#pragma unroll
+    for (int r = 0; r < kScatRows; ++r) q[r] = k[r] != kSentKey ? atomicAdd(cursor + kcol(k[r]), 1) : -1;
+#pragma unroll
+    for (int r = 0; r < kScatRows; ++r)
+      if (q[r] >= 0) inkeys[__ldg(rsoff + kcol(k[r])) + q[r]] = (uint32_t)(eb + r * 32 + lane);
+  }
+}
+
+// in-list entries: edge index e -> (source u = src[e] in place, e kept in ine[])
+__global__ void __launch_bounds__(256) k_in_resolve(uint32_t* ink, int* ine, const int* __restrict__ src,
+                                                    const int* __restrict__ rsoff, int n) {
+  const int total = __ldg(rsoff + n);
+  const int base = blockIdx.x * blockDim.x * 4 + threadIdx.x;
+  uint32_t e[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) { const int q = base + r * blockDim.x; e[r] = q < total ? ink[q] : 0u; }
+  int u[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) u[r] = base + r * (int)blockDim.x < total ? __ldg(src + e[r]) : 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int q = base + r * blockDim.x;
+    if (q < total) { ine[q] = (int)e[r]; ink[q] = (uint32_t)u[r]; }
   }
 }
 
@@ -84,7 +115,9 @@ struct MergeArgs {
   const int* off;           // pass 1 input: final offsets
   int2* arc;                // pass 1 output
   int* cap0;
-  int* colv;                // pass 1 output: dense column copy for the mate search
+  int* outslot;             // pass 1 output: slot of every out-half-arc (by sorted row position)
+  int* pend;                // pass 1 output: per slot, the edge index of one of its in-half-arcs (else -1)
+  const int* ine;           // edge index of every in-list entry
   int* wlist;               // vertices for the warp class
   int2* tasks;              // (vertex, chunk) tasks of the chunked class (> kMergeWarpMax)
   int* chunk_heads;         // distinct columns found by each chunk task
@@ -95,7 +128,6 @@ __device__ __forceinline__ void emit(const MergeArgs& a, int slot, uint32_t c, l
   if (sum > INT_MAX) { atomicExch(&a.ctrl->overflow, 1); sum = INT_MAX; }
   a.arc[slot] = make_int2((int)c, (int)sum);
   a.cap0[slot] = (int)sum;
-  a.colv[slot] = (int)c;
 }
 
 template <int PASS>
@@ -137,10 +169,12 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
         uint64_t k = a.outk[ob + i];
         if (kcol(k) != c) break;
         sum += kcap(k);
+        if (PASS == 1) a.outslot[ob + i] = slot0 + r;
         ++i;
       }
-      while (j < li && a.ink[ib + j] == c) ++j;
-      if (PASS == 1) emit(a, slot0 + r, c, sum);
+      int e_in = -1;
+      while (j < li && a.ink[ib + j] == c) { if (PASS == 1 && e_in < 0) e_in = a.ine[ib + j]; ++j; }
+      if (PASS == 1) { emit(a, slot0 + r, c, sum); a.pend[slot0 + r] = e_in; }
       ++r;
     }
     if (PASS == 0) a.mdeg[x] = r;
@@ -186,6 +220,13 @@ __device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int 
     if (lane == 0) pc = prev;
     bool head = valid && c != pc;
     unsigned hm = __ballot_sync(FULL, head);
+    if (PASS == 1 && valid) {
+      // slot of this output's run: the last head at or before this lane (a run without a
+      // head in this window continues the previous window's last slot)
+      const int slot = slot_base + heads + __popc(hm & (((1u << lane) - 1u) | (1u << lane))) - 1;
+      if (takeA) a.outslot[ob + i0 + i] = slot;
+      else a.pend[slot] = a.ine[ib + j0 + j];   // any in-half-arc of the run (parallel edges share the slot)
+    }
     if (PASS == 1 && head) {
       long long sum = 0;
       if (takeA) {
@@ -300,18 +341,23 @@ void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
   uint64_t* otmp = reinterpret_cast<uint64_t*>(a.arc);        // region C [0, 8m)
   int2* items = a.arc + m;                                    // region C [8m, 12m)
   int2* items_med = a.arc + m + m / 2 + 1;                    // region C [12m, 16m)
-  // out-keys and their sortedness flags were written by the validation pass (k_edges)
-  cudaMemsetAsync(a.cursor, 0, sizeof(int) * n, st);
-  int64_t threads = (m + 7) / 8;
-  if (m > 0) {
-    { k_inscatter<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(a.ro, a.col, n, m, a.rsoff, a.cursor, ink); note_launch(); }
-  }
+  // out-keys, their sortedness flags and the edge owners (src) were written by the
+  // validation pass (k_edges); rows not column-sorted are sorted first, so that the in-list
+  // entries can name out-half-arcs by their sorted position
   segmented_sort_filtered(outk, otmp, a.soff, (int)n, a.maxlen_out, a.need, a.ctrl, items, items_med, a.q0,
                           a.num_sms, st);
+  cudaMemsetAsync(a.cursor, 0, sizeof(int) * n, st);
+  if (m > 0) {
+    const int64_t sthreads = (m + kScatChunk - 1) / kScatChunk * 32;
+    { k_inscatter<<<(unsigned)((sthreads + T - 1) / T), T, 0, st>>>(outk, m, a.rsoff, a.cursor, ink); note_launch(); }
+  }
   segmented_sort32(ink, itmp, a.rsoff, (int)n, a.maxlen, a.ctrl, items, items_med, a.q0, a.num_sms, st);
+  if (m > 0) { k_in_resolve<<<(unsigned)((m + 1023) / 1024), T, 0, st>>>(ink, a.ine, a.src, a.rsoff, (int)n); note_launch(); }
+  cudaMemsetAsync(a.pend, 0xff, sizeof(int) * a.H, st);   // (src is dead: pend reuses its space)
   MergeArgs ma;
   ma.ooff = a.soff; ma.outk = outk; ma.ioff = a.rsoff; ma.ink = ink; ma.n = (int)n;
-  ma.mdeg = a.deg; ma.off = a.off; ma.arc = a.arc; ma.cap0 = a.cap0; ma.colv = a.colv;
+  ma.mdeg = a.deg; ma.off = a.off; ma.arc = a.arc; ma.cap0 = a.cap0;
+  ma.outslot = a.outslot; ma.pend = a.pend; ma.ine = a.ine;
   ma.wlist = a.q0; ma.tasks = a.mtasks; ma.chunk_heads = a.mheads; ma.ctrl = a.ctrl;
   cudaMemsetAsync(&a.ctrl->mlist_w, 0, 2 * sizeof(int), st);
   { k_merge_thread<0><<<gridcap(n, T, a.num_sms, 16), T, 0, st>>>(ma); note_launch(); }

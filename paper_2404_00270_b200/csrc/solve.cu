@@ -25,6 +25,7 @@
 // raised its excess from 0 (atomics on e make this unique) — a sparse compaction that
 // replaces the paper's full |V| rescan in every iteration (§8(a) A3).
 #include <climits>
+#include <cstdlib>
 
 #include "internal.h"
 #include "kernels.h"
@@ -146,6 +147,11 @@ constexpr int kSmallMax = 512;    // small-frontier mode: queues up to this size
 constexpr int kSmallDeg = 8;      // small-frontier mode: largest degree processed by one thread
 constexpr int kSB = 4;            // small-frontier mode: slots loaded per batch (independent loads)
 constexpr int kGapBins = 256;     // online gap: shared-memory bins for the lowest levels
+constexpr int kBuThread = 32;     // bottom-up BFS: vertices up to this many slots are scanned by one thread
+constexpr int kBuB = 8;           // bottom-up BFS: slots loaded per batch (independent loads)
+constexpr int kTdThread = 8;      // top-down BFS: frontier vertices up to this many slots are scanned by one thread
+constexpr int kTdPack = 4;        // top-down BFS: pack 32 frontier entries per warp when |frontier| >= kTdPack x warps
+constexpr int kRU = 4;            // push/relabel discharge: 32-slot groups loaded per iteration
 
 struct SharedState {
   int buf[kWarps][kBufCap];
@@ -244,8 +250,8 @@ __device__ __forceinline__ unsigned long long block_sum_u64(SharedState& S, unsi
   return t;  // thread 0
 }
 
-template <class Ops>
-__global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P, const Ops ops_in) {
+template <class Ops, int MINB>
+__global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams P, const Ops ops_in) {
   __shared__ SharedState S;
   Ops ops = ops_in;
   ops.init();
@@ -357,6 +363,15 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           else if (kind == PK_COMPACT) next = (qn + hc > 0) ? 1 : 0;
           const int md = ld_cg(&r->maxdeg);
           if (P.small_mode && P.schedule == 0 && next && hc == 0 && qn > 0 && qn <= kSmallMax && md <= kSmallDeg) flags |= 4;
+        }
+        {   // phase timing: release of the previous barrier -> this release, by phase kind
+          int bk = (kind == PK_BFS && G.bfs_bottom_up_prev) ? kPhBfsUp : kind;
+          if (bk >= 0 && bk < kPhBuckets && G.t_release) {
+            atomicAdd((unsigned long long*)&C->phase_ns[bk], now - G.t_release);
+            atomicAdd((unsigned long long*)&C->phase_cnt[bk], 1ull);
+          }
+          G.bfs_bottom_up_prev = (flags & 2) ? 1 : 0;
+          G.t_release = now;
         }
         b.x = target;
         b.y = (unsigned)qn;
@@ -564,11 +579,65 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
     st_bfs_arcs += d;
   };
 
+  // bottom-up BFS, one warp over slots [lo, hi) of a vertex: is there an out-arc with
+  // c_f > 0 into the current level?  kRU groups of 32 slots per iteration (all arc loads,
+  // then all label gathers), early exit per iteration.  All lanes call; warp-uniform result.
+  int level = 0;
+  auto bu_warp_scan = [&](const Seg& sg, int lo, int hi, int& scanned) -> bool {
+    for (int b = lo; b < hi; b += 32 * kRU) {
+      int col[kRU], cf[kRU];
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) {
+        const int i = b + j * 32 + lane;
+        col[j] = 0; cf[j] = 0;
+        if (i < hi) { int slot; ops.out_arc(sg, i, col[j], cf[j], slot); }
+      }
+      bool ok = false;
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) ok |= cf[j] > 0 && ld_cg_hint(P.h + col[j], pl) == level;
+      scanned += min(32 * kRU, hi - b);
+      if (__ballot_sync(FULL, ok)) return true;
+    }
+    return false;
+  };
+  // top-down BFS, one warp over in-arcs [lo, hi) of frontier vertex w: label every
+  // unlabelled u with c_f(u, w) > 0 (CAS; first finder appends u).  kRU groups per
+  // iteration: in-arc loads, then the c_f / label gathers, then the CASes, then the appends.
+  auto td_warp_scan = [&](const Seg& sg, int lo, int hi, const QueueOut& o, unsigned& fedges) {
+    for (int b = lo; b < hi; b += 32 * kRU) {
+      int u[kRU], cf[kRU], hu[kRU];
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) {
+        const int i = b + j * 32 + lane;
+        u[j] = 0; cf[j] = 0;
+        if (i < hi) ops.in_arc(sg, i, u[j], cf[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) hu[j] = cf[j] > 0 ? ld_cg_hint(P.h + u[j], pl) : -1;
+      bool found[kRU];
+#pragma unroll
+      for (int j = 0; j < kRU; ++j)   // sinks 0, sources N+1: never N; level(u) = level(w) + 1
+        found[j] = hu[j] == N && atomicCAS(P.h + u[j], N, level + 1) == N;
+      int dg[kRU];
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) dg[j] = found[j] ? ops.degree(u[j]) : 0;
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) {
+        if (!__ballot_sync(FULL, found[j])) continue;
+        unsigned fsum = warp_sum((unsigned)dg[j]);
+        if (lane == 0) fedges += fsum;
+        const bool huge = found[j] && dg[j] > kChunk;
+        if (huge) huge_append(u[j], dg[j], o);
+        warp_append(S, cnt, found[j] && !huge, u[j], o, dg[j]);
+      }
+    }
+  };
+
   enum { S_GR = 0, S_BFS = 1, S_COMPACT = 2, S_ROUND = 3, S_DONE = 4 };
   int phase = 1;          // 2: return the stranded excess to the sources (NEXT #2)
   bool converged = false; // phase ended by an exact GR with no active vertex
   long long rounds = 0;
-  int cur = 0, fb = 0, level = 0;
+  int cur = 0, fb = 0;
   int state = S_GR;
   unsigned small_epoch = 0;
 
@@ -661,6 +730,14 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           l_rounds += c_rounds; l_levels += c_levels;
           atomicAdd((unsigned long long*)&C->stats[ST_AVQ], (unsigned long long)c_avq);
           atomicAdd((unsigned long long*)&C->stats[ST_SMALL_PHASES], (unsigned long long)c_phases);
+          {
+            const unsigned long long now = globaltimer();
+            if (GC->pol.t_release) {
+              atomicAdd((unsigned long long*)&C->phase_ns[kPhSmall], now - GC->pol.t_release);
+              atomicAdd((unsigned long long*)&C->phase_cnt[kPhSmall], (unsigned long long)c_phases);
+            }
+            GC->pol.t_release = now;
+          }
           Resume& R = GC->res;
           R.state = state; R.qn = nn; R.hc = GC->small_hc; R.cur = cur; R.fb = fb; R.level = level;
           R.rounds = rounds;
@@ -739,40 +816,63 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           const int* qf = Q[fb];
           const HugeRec* hqf = HQ[fb];
           const int2* hcf = HC[fb];
-          int total = qn + hc;
-          for (int tk = gwarp; tk < total; tk += nwarps) {
-            int wv, lo, hi;
-            Seg sg;
-            if (tk < qn) {
-              wv = ld_cg(qf + tk);
-              sg = ops.seg(wv); lo = 0; hi = sg.deg();
-            } else {
-              int2 c = ld_cg(hcf + (tk - qn));
-              wv = ld_cg(&hqf[c.x].u);
-              sg = ops.seg(wv);
-              lo = c.y * kChunk; hi = min(sg.deg(), lo + kChunk);
-            }
-            if (lane == 0) st_bfs_arcs += hi - lo;
-            for (int b = lo; b < hi; b += 32) {
-              int i = b + lane;
-              bool found = false;
-              int u = 0, dg = 0;
-              if (i < hi) {
-                int cf;
-                ops.in_arc(sg, i, u, cf);
-                if (cf > 0 && ld_cg_hint(P.h + u, pl) == N) {   // sinks 0, sources N+1: never N
-                  if (atomicCAS(P.h + u, N, level + 1) == N) {   // level(u) = level(w) + 1
-                    found = true;
-                    dg = ops.degree(u);
-                  }
-                }
+          // frontier entries 32 per warp iteration: vertices with <= kBuThread slots are
+          // scanned by one THREAD each (kBuB in-arcs per batch, independent loads), larger
+          // ones by the whole warp (td_warp_scan), hub chunks one warp per chunk task
+          // (packing 32 entries per warp pays only when the frontier outnumbers the warps)
+          const int per = qn >= nwarps * kTdPack ? 32 : 1;
+          for (int base = gwarp * per; base < qn; base += nwarps * per) {
+            const int tk = base + (per == 32 ? lane : 0);
+            int wv = 0, dw = 0;
+            Seg sw;
+            if (tk < qn && (per == 32 || lane == 0)) { wv = ld_cg(qf + tk); sw = ops.seg(wv); dw = sw.deg(); }
+            const bool thr = per == 32 && tk < qn && dw <= kTdThread;
+            const int dthr = thr ? dw : 0;
+            if (thr) st_bfs_arcs += dw;   // per-thread partial (block-summed at the end)
+            for (int b0 = 0; __any_sync(FULL, b0 < dthr); b0 += kBuB) {
+              int u[kBuB], cf[kBuB];
+#pragma unroll
+              for (int j = 0; j < kBuB; ++j) {
+                u[j] = 0; cf[j] = 0;
+                if (b0 + j < dthr) ops.in_arc(sw, b0 + j, u[j], cf[j]);
               }
-              unsigned fsum = warp_sum((unsigned)dg);
-              if (lane == 0) fedges += fsum;
-              bool huge = found && dg > kChunk;
-              if (huge) huge_append(u, dg, o);
-              warp_append(S, cnt, found && !huge, u, o, dg);
+              int hu[kBuB];
+#pragma unroll
+              for (int j = 0; j < kBuB; ++j) hu[j] = cf[j] > 0 ? ld_cg_hint(P.h + u[j], pl) : -1;
+              bool found[kBuB];
+#pragma unroll
+              for (int j = 0; j < kBuB; ++j) found[j] = hu[j] == N && atomicCAS(P.h + u[j], N, level + 1) == N;
+              int dg[kBuB];
+#pragma unroll
+              for (int j = 0; j < kBuB; ++j) dg[j] = found[j] ? ops.degree(u[j]) : 0;
+#pragma unroll
+              for (int j = 0; j < kBuB; ++j) {
+                if (!__ballot_sync(FULL, found[j])) continue;
+                unsigned fsum = warp_sum((unsigned)dg[j]);
+                if (lane == 0) fedges += fsum;
+                const bool huge = found[j] && dg[j] > kChunk;
+                if (huge) huge_append(u[j], dg[j], o);
+                warp_append(S, cnt, found[j] && !huge, u[j], o, dg[j]);
+              }
             }
+            unsigned todo = __ballot_sync(FULL, tk < qn && !thr && (per == 32 || lane == 0));
+            while (todo) {
+              const int j = __ffs(todo) - 1;
+              todo &= todo - 1;
+              const int wj = __shfl_sync(FULL, wv, j);
+              Seg sg = ops.seg(wj);
+              const int d = sg.deg();
+              if (lane == 0) st_bfs_arcs += d;
+              td_warp_scan(sg, 0, d, o, fedges);
+            }
+          }
+          for (int t = gwarp; t < hc; t += nwarps) {
+            int2 c = ld_cg(hcf + t);
+            const int wv = ld_cg(&hqf[c.x].u);
+            Seg sg = ops.seg(wv);
+            const int lo = c.y * kChunk, hi = min(sg.deg(), lo + kChunk);
+            if (lane == 0) st_bfs_arcs += hi - lo;
+            td_warp_scan(sg, lo, hi, o, fedges);
           }
         } else {
           // ---- bottom-up: every unlabelled vertex v looks for an out-arc v -> w with
@@ -780,8 +880,35 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           for (int base = VLO + gwarp * 32; base < VHI; base += nwarps * 32) {
             int v = base + lane;
             int hv = v < VHI ? ld_cg_hint(P.h + v, pl) : -1;
-            unsigned todo = __ballot_sync(FULL, hv == N);
-            unsigned found_mask = 0;
+            // low-degree vertices (<= kBuThread slots, the bulk of a power-law graph): one
+            // THREAD per vertex, kBuB independent arc loads then kBuB label gathers per batch
+            // (early exit per batch); larger ones below, one warp per vertex
+            bool self_hit = false;
+            int dself = 0;
+            Seg sv;
+            if (hv == N) { sv = ops.seg(v); dself = sv.deg(); }
+            const bool thr = hv == N && dself <= kBuThread;
+            if (thr) {
+              int scanned = 0;
+              for (int b0 = 0; b0 < dself && !self_hit; b0 += kBuB) {
+                int col[kBuB], cf[kBuB];
+#pragma unroll
+                for (int j = 0; j < kBuB; ++j) {
+                  col[j] = 0; cf[j] = 0;
+                  if (b0 + j < dself) { int slot; ops.out_arc(sv, b0 + j, col[j], cf[j], slot); }
+                }
+                int hl[kBuB];
+#pragma unroll
+                for (int j = 0; j < kBuB; ++j) hl[j] = cf[j] > 0 ? ld_cg_hint(P.h + col[j], pl) : -1;
+#pragma unroll
+                for (int j = 0; j < kBuB; ++j) self_hit |= hl[j] == level;
+                scanned += min(kBuB, dself - b0);
+              }
+              st_bfs_arcs += scanned;   // per-thread partial; summed over the block at the end
+              if (self_hit) st_cg(P.h + v, level + 1);
+            }
+            unsigned todo = __ballot_sync(FULL, hv == N && !thr);
+            unsigned found_mask = __ballot_sync(FULL, self_hit);
             while (todo) {
               int j = __ffs(todo) - 1;
               todo &= todo - 1;
@@ -789,20 +916,9 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
               Seg sg = ops.seg(vv);
               int d = sg.deg();
               if (d > kChunk) continue;            // hubs: static chunk tasks below
-              bool hit = false;
               int scanned = 0;
-              for (int b = 0; b < d; b += 32) {
-                int i = b + lane;
-                bool ok = false;
-                if (i < d) {
-                  int col, cf, slot;
-                  ops.out_arc(sg, i, col, cf, slot);
-                  ok = cf > 0 && ld_cg_hint(P.h + col, pl) == level;
-                }
-                scanned += 32;
-                if (__ballot_sync(FULL, ok)) { hit = true; break; }
-              }
-              if (lane == 0) st_bfs_arcs += min(scanned, d);
+              const bool hit = bu_warp_scan(sg, 0, d, scanned);
+              if (lane == 0) st_bfs_arcs += scanned;
               if (hit) {
                 found_mask |= 1u << j;
                 if (lane == 0) st_cg(P.h + vv, level + 1);
@@ -822,21 +938,10 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
             if (ld_cg_hint(P.h + vv, pl) != N) continue;
             Seg sg = ops.seg(vv);
             int lo2 = hsk.y * kChunk, hi2 = min(sg.deg(), lo2 + kChunk);
-            bool hit = false;
             int scanned = 0;
-            for (int b = lo2; b < hi2; b += 32) {
-              int i = b + lane;
-              bool ok = false;
-              if (i < hi2) {
-                int col, cf, slot;
-                ops.out_arc(sg, i, col, cf, slot);
-                ok = cf > 0 && ld_cg_hint(P.h + col, pl) == level;
-              }
-              scanned += 32;
-              if (__ballot_sync(FULL, ok)) { hit = true; break; }
-            }
+            const bool hit = bu_warp_scan(sg, lo2, hi2, scanned);
             if (lane == 0) {
-              st_bfs_arcs += min(scanned, hi2 - lo2);
+              st_bfs_arcs += scanned;
               if (hit && atomicCAS(P.h + vv, N, level + 1) == N) {
                 huge_append(vv, sg.deg(), o);
                 fedges += sg.deg();
@@ -1001,28 +1106,33 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
           // by an exclusive prefix sum of the residual capacities in slot order.
           long long snap = eu;             // lower bound of e(u) (only u's warps decrease it)
           long long budget = eu;           // normal task: local budget
-          for (int b0 = lo; b0 < hi; b0 += 32) {
-            int i = b0 + lane;
-            int col = 0, cf = 0, slot = 0, hv = INT_MAX;
-            if (i < hi) {
-              ops.out_arc(sg, i, col, cf, slot);
-              if (cf > 0) {
-                hv = ld_cg_hint(P.h + col, pl);
-                unsigned long long cand = ((unsigned long long)(unsigned)hv << 32) | (unsigned)slot;
-                if (cand < best) { best = cand; bcf = cf; bcol = col; }
-              }
-            }
-            bool adm = cf > 0 && hv < hu;
-            unsigned am = __ballot_sync(FULL, adm);
-            if (!am) continue;
-            long long c = adm ? cf : 0;
-            long long incl = c;
+          // kRU groups of 32 slots per iteration: all arc loads, then all label gathers,
+          // then the pushes, then the appends, so each dependent memory step is paid once
+          // per 32*kRU slots instead of once per 32 (memory-level parallelism)
+          for (int b0 = lo; b0 < hi; b0 += 32 * kRU) {
+            int col[kRU], cf[kRU], slot[kRU], hv[kRU];
 #pragma unroll
-            for (int o2 = 1; o2 < 32; o2 <<= 1) {
-              long long y = __shfl_up_sync(FULL, incl, o2);
-              if (lane >= o2) incl += y;
+            for (int j = 0; j < kRU; ++j) {
+              const int i = b0 + j * 32 + lane;
+              col[j] = 0; cf[j] = 0; slot[j] = 0;
+              if (i < hi) ops.out_arc(sg, i, col[j], cf[j], slot[j]);
             }
-            long long want = __shfl_sync(FULL, incl, 31);
+#pragma unroll
+            for (int j = 0; j < kRU; ++j) hv[j] = cf[j] > 0 ? ld_cg_hint(P.h + col[j], pl) : INT_MAX;
+            long long want = 0;            // admissible capacity of the whole super-group
+            unsigned amask = 0;            // groups with an admissible arc
+#pragma unroll
+            for (int j = 0; j < kRU; ++j) {
+              if (cf[j] > 0) {
+                unsigned long long cand = ((unsigned long long)(unsigned)hv[j] << 32) | (unsigned)slot[j];
+                if (cand < best) { best = cand; bcf = cf[j]; bcol = col[j]; }
+              }
+              const bool adm = cf[j] > 0 && hv[j] < hu;
+              if (__ballot_sync(FULL, adm)) amask |= 1u << j;
+              want += adm ? (long long)cf[j] : 0;
+            }
+            if (!amask) continue;
+            want = warp_sum(want);
             long long avail;
             if (hidx < 0) {
               avail = budget;
@@ -1033,22 +1143,47 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
               avail = snap - got;
               if (avail < 0) avail = 0;
             }
-            long long excl = incl - c;
-            long long d = adm ? (avail - excl < c ? avail - excl : c) : 0;
-            bool app = false;
-            if (d > 0) {
-              ops.push(slot, (int)d);
-              long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col), (unsigned long long)d);
-              app = old_v == 0 && ld_term(P.term + col) == 0;
-              ++st_push;
+            // split avail over the admissible arcs in slot order (group-major, then lane)
+            long long before = 0;          // admissible capacity of the earlier groups
+            long long oldv[kRU];
+#pragma unroll
+            for (int j = 0; j < kRU; ++j) {
+              oldv[j] = -1;
+              if (!((amask >> j) & 1u)) continue;
+              const bool adm = cf[j] > 0 && hv[j] < hu;
+              const long long c = adm ? cf[j] : 0;
+              long long incl = c;
+#pragma unroll
+              for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                long long y = __shfl_up_sync(FULL, incl, o2);
+                if (lane >= o2) incl += y;
+              }
+              const long long excl = before + incl - c;
+              before += __shfl_sync(FULL, incl, 31);
+              const long long d = adm ? (avail - excl < c ? avail - excl : c) : 0;
+              if (d > 0) {
+                ops.push(slot[j], (int)d);
+                oldv[j] = (long long)atomicAdd((unsigned long long*)(P.e + col[j]), (unsigned long long)d);
+                ++st_push;
+              }
             }
-            long long used = want < avail ? want : avail;
+            const long long used = want < avail ? want : avail;
             pushed += used;
             budget -= used;
-            int dgv = app ? ops.degree(col) : 0;
-            bool hugev = app && dgv > kChunk;
-            if (hugev) huge_append(col, dgv, o);
-            warp_append(S, cnt, app && !hugev, col, o, dgv);
+            // a push that raised e(v) from 0 appends v (exactly once, atomics on e)
+            bool app[kRU];
+#pragma unroll
+            for (int j = 0; j < kRU; ++j) app[j] = oldv[j] == 0 && ld_term(P.term + col[j]) == 0;
+            int dgv[kRU];
+#pragma unroll
+            for (int j = 0; j < kRU; ++j) dgv[j] = app[j] ? ops.degree(col[j]) : 0;
+#pragma unroll
+            for (int j = 0; j < kRU; ++j) {
+              if (!((amask >> j) & 1u)) continue;
+              const bool hugev = app[j] && dgv[j] > kChunk;
+              if (hugev) huge_append(col[j], dgv[j], o);
+              warp_append(S, cnt, app[j] && !hugev, col[j], o, dgv[j]);
+            }
             if (hidx < 0 && budget <= 0) break;
           }
         }
@@ -1176,12 +1311,25 @@ __global__ void __launch_bounds__(kSolveThreads, 2) k_solve(const SolveParams P,
 }
 
 // ------------------------------------------------------------------ host launch
+// Two register budgets: MINB = 2 (64 registers, 2 CTAs / 32 warps per SM, some spills) and
+// MINB = 1 (128 registers, 1 CTA / 16 warps per SM, no spills).  WBPR_SOLVE_MINB picks one
+// (default kSolveMinBlocks).
+static int solve_minb() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("WBPR_SOLVE_MINB");
+    v = (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : kSolveMinBlocks;
+  }
+  return v;
+}
+
+template <class Ops> static const void* solve_fn() {
+  return solve_minb() == 1 ? (const void*)k_solve<Ops, 1> : (const void*)k_solve<Ops, 2>;
+}
+
 int solve_max_blocks_per_sm(int layout, int threads) {
   int b = 0;
-  if (layout == 0)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_solve<BcsrOps>, threads, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_solve<RcsrOps>, threads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, layout == 0 ? solve_fn<BcsrOps>() : solve_fn<RcsrOps>(), threads, 0);
   return b;
 }
 
@@ -1190,11 +1338,11 @@ cudaError_t launch_solve(const SolveParams& p, int blocks, int threads, cudaStre
   if (p.layout == 0) {
     BcsrOps o{p.off, p.arc, p.mate};
     void* args[] = {(void*)&p, (void*)&o};
-    return cudaLaunchCooperativeKernel((void*)k_solve<BcsrOps>, dim3(blocks), dim3(threads), args, 0, st);
+    return cudaLaunchCooperativeKernel(solve_fn<BcsrOps>(), dim3(blocks), dim3(threads), args, 0, st);
   } else {
     RcsrOps o{p.off, p.arc, p.roff, p.rarc, p.bcf, p.Mf};
     void* args[] = {(void*)&p, (void*)&o};
-    return cudaLaunchCooperativeKernel((void*)k_solve<RcsrOps>, dim3(blocks), dim3(threads), args, 0, st);
+    return cudaLaunchCooperativeKernel(solve_fn<RcsrOps>(), dim3(blocks), dim3(threads), args, 0, st);
   }
 }
 

@@ -56,10 +56,14 @@ class Stats(ctypes.Structure):
         ("build_ms", ctypes.c_float), ("solve_ms", ctypes.c_float), ("extract_ms", ctypes.c_float),
         ("total_ms", ctypes.c_float), ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int64), ("t_barrier_ns", ctypes.c_int64), ("t_flush_ns", ctypes.c_int64),
-        ("t_round_ns", ctypes.c_int64)]
+        ("t_round_ns", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 9), ("phase_count", ctypes.c_int64 * 9)]
 
     def as_dict(self):
-        return {f[0]: getattr(self, f[0]) for f in self._fields_}
+        d = {}
+        for f in self._fields_:
+            v = getattr(self, f[0])
+            d[f[0]] = list(v) if isinstance(v, ctypes.Array) else v
+        return d
 
 
 class Residual(ctypes.Structure):
