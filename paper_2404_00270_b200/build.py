@@ -43,16 +43,20 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
-    stamp = os.path.join(OBJ, "digest")
-    dg = _digest()
-    if not force and os.path.exists(OUT) and os.path.exists(stamp) and open(stamp).read() == dg:
-        return OUT
+def build(force: bool = False, verbose: bool = False, defines=(), variant: str = "") -> str:
+    """variant/defines: an experiment build (extra -D flags) into libwbpr_<variant>.so,
+    loaded when WBPR_LIB points at it; the default build is libwbpr.so."""
+    obj_dir = OBJ if not variant else os.path.join(OBJ, variant)
+    out = OUT if not variant else os.path.join(HERE, f"libwbpr_{variant}.so")
+    os.makedirs(obj_dir, exist_ok=True)
+    stamp = os.path.join(obj_dir, "digest")
+    dg = _digest() + " ".join(defines)
+    if not force and os.path.exists(out) and os.path.exists(stamp) and open(stamp).read() == dg:
+        return out
 
     def comp(src):
-        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-        cmd = [NVCC] + ARCH + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+        obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
+        cmd = [NVCC] + ARCH + FLAGS + list(defines) + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -63,16 +67,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         for _, err in results:
             sys.stderr.write(err)
-    tmp = OUT + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + [o for o, _ in results]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
+    os.replace(tmp, out)
     with open(stamp, "w") as f:
         f.write(dg)
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    var = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--variant=")), "")
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, variant=var))

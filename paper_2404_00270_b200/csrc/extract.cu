@@ -21,34 +21,41 @@ __global__ void k_bitmap(const int* __restrict__ h, int n, int N, uint32_t* bitm
   }
 }
 
-constexpr int kCutEdges = 8;
-
-__global__ void k_cutcap(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
-                         const int32_t* __restrict__ cap, int64_t n, int64_t m, const int* __restrict__ h, int N,
-                         const int64_t* __restrict__ vbase, int k, long long* cut) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t i0 = t * kCutEdges;
-  if (i0 >= m) return;
+// One warp per kCutChunk consecutive input edges as rows of 32 (coalesced col/cap loads,
+// owners by warp_owner); h(v) is gathered only for edges leaving S*.
+constexpr int kCutChunk = 32 * 64;
+__global__ void __launch_bounds__(256) k_cutcap(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
+                                                const int32_t* __restrict__ cap, int64_t n, int64_t m,
+                                                const int* __restrict__ h, int N, const int64_t* __restrict__ vbase,
+                                                int k, long long* cut) {
+  const int lane = lane_id();
+  const int64_t E0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kCutChunk;
+  if (E0 >= m) return;
+  const int64_t E1 = E0 + kCutChunk < m ? E0 + kCutChunk : m;
   int64_t lo = 0, hi = n;
-  while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (__ldg(ro + mid) <= i0) lo = mid; else hi = mid; }
-  int64_t u = lo;
-  int inst = 0;
-  { int a = 0, b = k; while (b - a > 1) { int mid = (a + b) >> 1; if (__ldg(vbase + mid) <= u) a = mid; else b = mid; } inst = a; }
+  while (hi - lo > 1) { int64_t mid = (lo + hi) >> 1; if (__ldg(ro + mid) <= E0) lo = mid; else hi = mid; }
+  int ucur = (int)lo;
+  int inst = -1;           // instance of the lane's accumulator
+  int64_t ilo = 0, ihi = 0;
   long long acc = 0;
-  int64_t i1 = i0 + kCutEdges < m ? i0 + kCutEdges : m;
-  int hu = ld_cg(h + u);
-  for (int64_t i = i0; i < i1; ++i) {
-    while (__ldg(ro + u + 1) <= i) {
-      ++u;
-      hu = ld_cg(h + u);
-      if (u >= __ldg(vbase + inst + 1)) {
+  for (int64_t eb = E0; eb < E1; eb += 32) {
+    const int64_t i = eb + lane;
+    const bool ok = i < E1;
+    const int u = warp_owner(ro, (int)n, ucur, ok ? i : E1 - 1);
+    ucur = __shfl_sync(FULL, u, 31);
+    if (!ok) continue;
+    const int v = __ldg(col + i);
+    const int c = __ldg(cap + i);
+    if (ld_cg(h + u) >= N && ld_cg(h + v) < N) {
+      if (u < ilo || u >= ihi) {
         if (acc) atomicAdd((unsigned long long*)(cut + inst), (unsigned long long)acc);
         acc = 0;
-        while (u >= __ldg(vbase + inst + 1)) ++inst;
+        int a = 0, b = k;
+        while (b - a > 1) { int mid = (a + b) >> 1; if (__ldg(vbase + mid) <= u) a = mid; else b = mid; }
+        inst = a; ilo = __ldg(vbase + a); ihi = __ldg(vbase + a + 1);
       }
+      acc += c;
     }
-    int v = col[i];
-    if (hu >= N && ld_cg(h + v) < N) acc += cap[i];
   }
   if (acc) atomicAdd((unsigned long long*)(cut + inst), (unsigned long long)acc);
 }
@@ -70,7 +77,7 @@ void extract_results(const SolveParams& p, const int64_t* ro, const int32_t* col
   }
   cudaMemsetAsync(inst_cut, 0, sizeof(long long) * k, st);
   if (m > 0) {
-    int64_t threads = (m + kCutEdges - 1) / kCutEdges;
+    int64_t threads = (m + kCutChunk - 1) / kCutChunk * 32;
     { k_cutcap<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(ro, col, cap, p.n, m, p.h, p.n, vbase, k, inst_cut); note_launch(); }
   }
   { k_flows<<<(k + T - 1) / T, T, 0, st>>>(p.e, p.snk, k, inst_flow); note_launch(); }

@@ -9,7 +9,10 @@
 
 namespace wbpr {
 
-constexpr int kChunk = 1024;       // slots per warp task; vertices with more slots are "huge"
+#ifndef WBPR_CHUNK
+#define WBPR_CHUNK 1024
+#endif
+constexpr int kChunk = WBPR_CHUNK; // slots per warp task; vertices with more slots are "huge"
 constexpr int kSortTile = 4096;    // CTA shared-memory sort tile (64-bit keys)
 constexpr int kScanTile = 4096;    // elements per scan tile
 constexpr int kMaxInst = 1 << 20;  // batch instances

@@ -62,11 +62,12 @@ __global__ void k_outkeys(const int64_t* __restrict__ ro, const int32_t* __restr
 // the source u, since rows are stored in vertex order); k_in_resolve then turns e into
 // u and keeps e beside it, so the merge can pair both half-arcs of the edge (mate[]).
 // One warp per kScatChunk consecutive edges as rows of 32 (coalesced loads); the
-// kScatRows cursor atomics of a lane are issued back to back.
+// kScatRows cursor atomics of a lane are issued back to back; the cursors start at the
+// in-list offsets, so an atomic returns the absolute position.
 constexpr int kScatRows = 8;
 constexpr int kScatChunk = 32 * kScatRows * 8;
-__global__ void __launch_bounds__(256) k_inscatter(const uint64_t* __restrict__ outk, int64_t m,
-                                                   const int* __restrict__ rsoff, int* cursor, uint32_t* inkeys) {
+__global__ void __launch_bounds__(256) k_inscatter(const uint64_t* __restrict__ outk, int64_t m, int* cursor,
+                                                   uint32_t* inkeys) {
   const int lane = lane_id();
   const int64_t E0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kScatChunk;
   if (E0 >= m) return;
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(256) k_inscatter(const uint64_t* __restrict__ 
     for (int r = 0; r < kScatRows; ++r) q[r] = k[r] != kSentKey ? atomicAdd(cursor + kcol(k[r]), 1) : -1;
 #pragma unroll
     for (int r = 0; r < kScatRows; ++r)
-      if (q[r] >= 0) inkeys[__ldg(rsoff + kcol(k[r])) + q[r]] = (uint32_t)(eb + r * 32 + lane);
+      if (q[r] >= 0) inkeys[q[r]] = (uint32_t)(eb + r * 32 + lane);
   }
 }
 
@@ -159,21 +160,30 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
     if (x >= a.n || big) continue;
     int i = 0, j = 0, r = 0;
     int slot0 = PASS == 1 ? __ldg(a.off + x) : 0;
+    // two-pointer merge; each element is loaded once, the next head of a list is loaded as
+    // soon as its current one is consumed (one dependent load per consumed element)
+    uint64_t ka = lo > 0 ? a.outk[ob] : kSentKey;
+    uint32_t kb = li > 0 ? a.ink[ib] : kInf;
+    int eb = (PASS == 1 && li > 0) ? a.ine[ib] : 0;
     while (true) {
-      uint32_t co = i < lo ? kcol(a.outk[ob + i]) : kInf;
-      uint32_t ci = j < li ? a.ink[ib + j] : kInf;
-      uint32_t c = co < ci ? co : ci;
+      uint32_t ca = kcol(ka);
+      const uint32_t c = ca < kb ? ca : kb;
       if (c == kInf) break;
       long long sum = 0;
-      while (i < lo) {
-        uint64_t k = a.outk[ob + i];
-        if (kcol(k) != c) break;
-        sum += kcap(k);
+      while (ca == c) {
+        sum += kcap(ka);
         if (PASS == 1) a.outslot[ob + i] = slot0 + r;
         ++i;
+        ka = i < lo ? a.outk[ob + i] : kSentKey;
+        ca = kcol(ka);
       }
       int e_in = -1;
-      while (j < li && a.ink[ib + j] == c) { if (PASS == 1 && e_in < 0) e_in = a.ine[ib + j]; ++j; }
+      while (kb == c) {
+        if (e_in < 0) e_in = eb;
+        ++j;
+        kb = j < li ? a.ink[ib + j] : kInf;
+        if (PASS == 1) eb = j < li ? a.ine[ib + j] : 0;
+      }
       if (PASS == 1) { emit(a, slot0 + r, c, sum); a.pend[slot0 + r] = e_in; }
       ++r;
     }
@@ -346,10 +356,10 @@ void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
   // entries can name out-half-arcs by their sorted position
   segmented_sort_filtered(outk, otmp, a.soff, (int)n, a.maxlen_out, a.need, a.ctrl, items, items_med, a.q0,
                           a.num_sms, st);
-  cudaMemsetAsync(a.cursor, 0, sizeof(int) * n, st);
+  cudaMemcpyAsync(a.cursor, a.rsoff, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
   if (m > 0) {
     const int64_t sthreads = (m + kScatChunk - 1) / kScatChunk * 32;
-    { k_inscatter<<<(unsigned)((sthreads + T - 1) / T), T, 0, st>>>(outk, m, a.rsoff, a.cursor, ink); note_launch(); }
+    { k_inscatter<<<(unsigned)((sthreads + T - 1) / T), T, 0, st>>>(outk, m, a.cursor, ink); note_launch(); }
   }
   segmented_sort32(ink, itmp, a.rsoff, (int)n, a.maxlen, a.ctrl, items, items_med, a.q0, a.num_sms, st);
   if (m > 0) { k_in_resolve<<<(unsigned)((m + 1023) / 1024), T, 0, st>>>(ink, a.ine, a.src, a.rsoff, (int)n); note_launch(); }

@@ -6,10 +6,10 @@
 //
 // Segment classes (lengths from 1 to ~1.6e5 at R-MAT scale 22):
 //   len <= 32         one warp per segment, rank sort in registers (32 shuffles)
-//   32 < len <= 256   one warp per segment, register bitonic network sized to the
-//                     length (2/4/8 keys per lane; shuffles for the cross-lane stages,
-//                     no shared memory, no barriers)
-//   256 < len <= 4096 one 512-thread CTA: each warp sorts a 256-key chunk in
+//   32 < len <= 1024  one warp per segment (<= 512 for 64-bit keys), register bitonic
+//                     network sized to the length (2..32 keys per lane; shuffles for the
+//                     cross-lane stages, no shared memory, no barriers)
+//   ... len <= 4096   one 512-thread CTA: each warp sorts a 256-key chunk in
 //                     registers, then merge-path passes in shared memory
 //   len > 4096        4096-key chunks sorted as above, then log2(len/4096) merge
 //                     passes in global memory (co-rank search, 8 outputs per thread),
@@ -22,6 +22,7 @@ namespace wbpr {
 
 constexpr int kTileThreads = 512;
 constexpr int kMedLen = 256;   // warp register sort up to this length
+constexpr int kWarpMergeMax = 1024;   // warp chunk-sort + shared-memory merge up to this length (32-bit keys)
 
 template <typename K> __device__ __forceinline__ K key_max() { return (K)~(K)0; }
 
@@ -103,6 +104,11 @@ __device__ __forceinline__ void warp_sort_segment(K* keys, int beg, int len, int
   }
 }
 
+// Longest segment sorted by one warp (32-bit keys: <= 1024 keys as 256-key register
+// bitonic chunks merged in warp-private shared memory; 64-bit keys: <= 256 in registers).
+// Longer segments go to the CTA tile sort, whose merge passes need several warps to pay off.
+template <typename K> constexpr int warp_sort_max() { return sizeof(K) == 4 ? kWarpMergeMax : kMedLen; }
+
 template <typename K>
 __global__ void __launch_bounds__(256) k_sort_med(K* keys, const int2* __restrict__ items, const int* count) {
   const int nitems = *count;
@@ -111,6 +117,7 @@ __global__ void __launch_bounds__(256) k_sort_med(K* keys, const int2* __restric
   int lane = lane_id();
   for (int it = wg; it < nitems; it += nw) {
     int2 item = items[it];
+    if (item.y > kMedLen) continue;   // (32-bit keys) k_sort_wm
     if (item.y <= 64) warp_sort_segment<K, 2>(keys, item.x, item.y, lane);
     else if (item.y <= 128) warp_sort_segment<K, 4>(keys, item.x, item.y, lane);
     else warp_sort_segment<K, 8>(keys, item.x, item.y, lane);
@@ -120,12 +127,12 @@ __global__ void __launch_bounds__(256) k_sort_med(K* keys, const int2* __restric
 // Enumerate sort items: 32 < len <= 256 -> warp items; 256 < len <= tile -> CTA item;
 // longer segments -> ceil(len/tile) CTA chunk items and the `big` list.
 __global__ void k_sort_items(const int* __restrict__ off, int nseg, const uint8_t* __restrict__ need,
-                             int2* items, int2* items_med, int* big, Ctrl* ctrl) {
+                             int2* items, int2* items_med, int* big, Ctrl* ctrl, int medmax) {
   for (int sgi = blockIdx.x * blockDim.x + threadIdx.x; sgi < nseg; sgi += gridDim.x * blockDim.x) {
     if (need && !need[sgi]) continue;
     int beg = off[sgi], len = off[sgi + 1] - beg;
     if (len <= 32) continue;
-    if (len <= kMedLen) {
+    if (len <= medmax) {
       items_med[atomicAdd(&ctrl->sort_items_med, 1)] = make_int2(beg, len);
       continue;
     }
@@ -150,6 +157,58 @@ __device__ __forceinline__ int co_rank(int k, const K* A, int la, const K* B, in
     if (A[i] <= B[k - i - 1]) lo = i + 1; else hi = i;
   }
   return lo;
+}
+
+// 256 < len <= kWarpMergeMax (32-bit keys): one warp sorts the 256-key chunks of the
+// segment (padded to a power of two) with the register bitonic network, then merges them
+// pairwise in its own shared memory (merge path: each lane emits a run of consecutive
+// outputs from its co-rank) and writes the result back coalesced.
+__global__ void __launch_bounds__(256) k_sort_wm(uint32_t* keys, const int2* __restrict__ items, const int* count) {
+  extern __shared__ __align__(16) uint32_t wsm[];
+  uint32_t* const A0 = wsm + warp_id() * 2 * kWarpMergeMax;
+  uint32_t* const B0 = A0 + kWarpMergeMax;
+  const int nitems = *count;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int lane = lane_id();
+  for (int it = wg; it < nitems; it += nw) {
+    const int2 item = items[it];
+    const int beg = item.x, len = item.y;
+    if (len <= kMedLen) continue;      // k_sort_med
+    const int total = len <= 512 ? 512 : kWarpMergeMax;
+    for (int c = 0; c < total / kMedLen; ++c) {
+      uint32_t r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = c * kMedLen + j * 32 + lane;
+        r[j] = e < len ? keys[beg + e] : 0xffffffffu;
+      }
+      warp_bitonic<uint32_t, 8>(r, lane);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) A0[c * kMedLen + j * 32 + lane] = r[j];
+    }
+    __syncwarp();
+    uint32_t* src = A0;
+    uint32_t* dst = B0;
+    const int per = total / 32;
+    for (int wd = kMedLen; wd < total; wd <<= 1) {
+      const int kk = lane * per;
+      const int pair0 = kk / (2 * wd) * (2 * wd);
+      const uint32_t* SA = src + pair0;
+      const uint32_t* SB = SA + wd;
+      const int k = kk - pair0;
+      int i = co_rank<uint32_t>(k, SA, wd, SB, wd);
+      int j = k - i;
+      for (int q = 0; q < per; ++q) {
+        const bool takeA = j >= wd || (i < wd && SA[i] <= SB[j]);
+        dst[kk + q] = takeA ? SA[i++] : SB[j++];
+      }
+      __syncwarp();
+      uint32_t* t = src; src = dst; dst = t;
+    }
+    for (int e = lane; e < len; e += 32) keys[beg + e] = src[e];
+    __syncwarp();
+  }
 }
 
 template <typename K>
@@ -261,10 +320,18 @@ void segmented_sort_t(K* keys, K* tmp, const int* off, int nseg, int maxlen, con
   {
     int64_t blocks = (nseg + 255) / 256;
     if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
-    { k_sort_items<<<(unsigned)blocks, 256, 0, st>>>(off, nseg, need, items, items_med, big, ctrl); note_launch(); }
+    { k_sort_items<<<(unsigned)blocks, 256, 0, st>>>(off, nseg, need, items, items_med, big, ctrl, warp_sort_max<K>()); note_launch(); }
   }
   { k_sort_med<K><<<num_sms * 16, 256, 0, st>>>(keys, items_med, &ctrl->sort_items_med); note_launch(); }
-  if (maxlen <= kMedLen) return;
+  if constexpr (sizeof(K) == 4) {
+    if (maxlen > kMedLen) {
+      const int smem = 8 * 2 * kWarpMergeMax * (int)sizeof(uint32_t);
+      cudaFuncSetAttribute(k_sort_wm, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      k_sort_wm<<<num_sms * 3, 256, smem, st>>>(reinterpret_cast<uint32_t*>(keys), items_med, &ctrl->sort_items_med);
+      note_launch();
+    }
+  }
+  if (maxlen <= warp_sort_max<K>()) return;
   {
     const int smem = 2 * kSortTile * (int)sizeof(K);
     cudaFuncSetAttribute(k_sort_tile<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

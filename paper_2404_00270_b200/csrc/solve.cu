@@ -151,7 +151,10 @@ constexpr int kBuThread = 32;     // bottom-up BFS: vertices up to this many slo
 constexpr int kBuB = 8;           // bottom-up BFS: slots loaded per batch (independent loads)
 constexpr int kTdThread = 8;      // top-down BFS: frontier vertices up to this many slots are scanned by one thread
 constexpr int kTdPack = 4;        // top-down BFS: pack 32 frontier entries per warp when |frontier| >= kTdPack x warps
-constexpr int kRU = 4;            // push/relabel discharge: 32-slot groups loaded per iteration
+#ifndef WBPR_RU
+#define WBPR_RU 4
+#endif
+constexpr int kRU = WBPR_RU;      // push/relabel discharge: 32-slot groups loaded per iteration
 
 struct SharedState {
   int buf[kWarps][kBufCap];
@@ -886,6 +889,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             bool self_hit = false;
             int dself = 0;
             Seg sv;
+            sv.fb = sv.fe = sv.rb = sv.re = 0;
             if (hv == N) { sv = ops.seg(v); dself = sv.deg(); }
             const bool thr = hv == N && dself <= kBuThread;
             if (thr) {
@@ -913,7 +917,9 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               int j = __ffs(todo) - 1;
               todo &= todo - 1;
               int vv = base + j;
-              Seg sg = ops.seg(vv);
+              Seg sg;                               // lane j loaded it above
+              sg.fb = __shfl_sync(FULL, sv.fb, j); sg.fe = __shfl_sync(FULL, sv.fe, j);
+              sg.rb = __shfl_sync(FULL, sv.rb, j); sg.re = __shfl_sync(FULL, sv.re, j);
               int d = sg.deg();
               if (d > kChunk) continue;            // hubs: static chunk tasks below
               int scanned = 0;

@@ -79,10 +79,11 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2404_00270_b200.build` "
+    path = os.environ.get("WBPR_LIB", LIB_PATH)   # experiment builds (build.py --variant=...)
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -m paper_2404_00270_b200.build` "
                           "(the CUDA path has no fallback)")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     lib.wbpr_default_options.argtypes = [ctypes.POINTER(Options)]
     lib.wbpr_workspace_size.argtypes = [i64, i64, i32, ctypes.POINTER(Options), ctypes.POINTER(ctypes.c_size_t)]
