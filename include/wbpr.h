@@ -197,10 +197,14 @@ wbpr_status wbpr_bipartite_match(int64_t nL, int64_t nR, int64_t E, const int32_
                                  void* stream);
 
 /* Debug/test view of the residual state left in a workspace by the last solve.
- * All pointers are DEVICE pointers into the workspace.  BCSR: off/arc/mate/cap0 with
- * arc[p] = {col, cf}.  RCSR: foff/farc/cap0 (forward), roff/rarc (rarc[q] = {col,
- * flow_idx}), bcf (backward cf per forward arc).  e = excess (int64[n]),
- * h = heights (int32[n], >= n means source side). */
+ * All pointers are DEVICE pointers into the workspace.  BCSR (gapped): vertex u's
+ * segment is slots [seg[2u], seg[2u+1]) of arc/mate/cap0, which span M = 2m slots;
+ * segments appear in vertex order and the slots between one segment's end and the next
+ * one's begin are unused (they absorb the merged parallel / antiparallel half-arcs, so
+ * no counting pass is needed; off = NULL).  arc[p] = {col, cf}; mate[p] = slot of the
+ * reverse arc.  RCSR: foff/farc/cap0 (forward), roff/rarc (rarc[q] = {col, flow_idx}),
+ * bcf (backward cf per forward arc).  e = excess (int64[n]), h = heights (int32[n],
+ * >= n means source side). */
 typedef struct wbpr_residual {
   int32_t layout;
   int64_t n, M, Mf;
@@ -213,6 +217,7 @@ typedef struct wbpr_residual {
   const int32_t* bcf;   /* RCSR [Mf] */
   const int64_t* e;
   const int32_t* h;
+  const int32_t* seg;   /* BCSR: int2 {begin, end} per vertex [n] (gapped segments) */
 } wbpr_residual;
 wbpr_status wbpr_residual_view(const void* workspace, wbpr_residual* view);
 

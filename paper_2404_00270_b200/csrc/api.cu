@@ -128,6 +128,7 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
   a.src = at<int>(W.base, L.regA + 8 * (size_t)L.m);
   a.pend = at<int>(W.base, L.regA + 8 * (size_t)L.m);
   a.outslot = at<int>(W.base, L.regD);
+  a.seg = at<int2>(W.base, L.seg);
 
   build_validate(a, st);
   CK(cudaGetLastError());
@@ -175,6 +176,9 @@ void register_view(const Ws& W, int layout, int M, int Mf) {
   v.arc = at<int>(W.base, L.regC);
   v.cap0 = at<int>(W.base, L.regB + L.bcap0);
   if (layout == WBPR_LAYOUT_BCSR) {
+    v.off = nullptr;                       // gapped layout: segments by seg[u] = {begin, end}
+    v.seg = at<int32_t>(W.base, L.seg);
+    v.M = 2 * L.m;                         // extent of the slot space (arc/mate/cap0 length)
     v.mate = at<int>(W.base, L.regB);
   } else {
     v.roff = at<int>(W.base, L.roff);
@@ -293,6 +297,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.ctrl = W.ctrl;
   P.n = (int)n; P.k = k; P.layout = opt.layout; P.M = 0; P.Mf = Mf;
   P.off = at<int>(ws, L.off);
+  P.seg = at<int2>(ws, L.seg);
   P.arc = at<int2>(ws, L.regC);
   P.mate = at<int>(ws, L.regB);
   P.roff = at<int>(ws, L.roff);
@@ -606,6 +611,7 @@ wbpr_status wbpr_bipartite_match(int64_t nL, int64_t nR, int64_t E, const int32_
   SolveParams P{};
   P.layout = opt.layout;
   P.off = at<int>(workspace, L.off);
+  P.seg = at<int2>(workspace, L.seg);
   P.arc = at<int2>(workspace, L.regC);
   P.roff = at<int>(workspace, L.roff);
   P.rarc = at<int2>(workspace, L.regC + 8 * (size_t)m);

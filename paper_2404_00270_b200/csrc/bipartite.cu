@@ -52,11 +52,11 @@ __global__ void k_bip_scatter(const int32_t* __restrict__ l, const int32_t* __re
   }
 }
 
-__global__ void k_bip_extract_bcsr(const int* __restrict__ off, const int2* __restrict__ arc, int64_t nL, int64_t nR,
+__global__ void k_bip_extract_bcsr(const int2* __restrict__ seg, const int2* __restrict__ arc, int64_t nL, int64_t nR,
                                    int32_t* match) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nR; j += (int64_t)gridDim.x * blockDim.x) {
     int x = (int)(1 + nL + j);
-    int b = off[x], e = off[x + 1];
+    int b = seg[x].x, e = seg[x].y;
     if (e <= b) continue;
     int2 last = ld_cg(arc + e - 1);                        // column t sorts last
     if (last.x != (int)(nL + nR + 1) || last.y != 0) continue;   // x -> t not saturated
@@ -89,7 +89,7 @@ void bip_extract(const SolveParams& p, int64_t nL, int64_t nR, int32_t* match_of
   cudaMemsetAsync(match_of_left, 0xff, sizeof(int32_t) * nL, st);
   unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nR + T - 1) / T, num_sms * 32));
   if (nR <= 0) return;
-  if (p.layout == 0) { k_bip_extract_bcsr<<<g, T, 0, st>>>(p.off, p.arc, nL, nR, match_of_left); note_launch(); }
+  if (p.layout == 0) { k_bip_extract_bcsr<<<g, T, 0, st>>>(p.seg, p.arc, nL, nR, match_of_left); note_launch(); }
   else { k_bip_extract_rcsr<<<g, T, 0, st>>>(p.off, p.arc, p.roff, p.rarc, p.bcf, nL, nR, match_of_left); note_launch(); }
 }
 

@@ -225,8 +225,8 @@ __global__ void k_colcopy(const int2* __restrict__ arc, const Ctrl* ctrl, int* c
 // written from both sides (same values); every slot is written by itself or its partner.
 constexpr int kMatePerThread = 4;
 __global__ void __launch_bounds__(256) k_mate(const int* __restrict__ pend, const int* __restrict__ outslot,
-                                              const Ctrl* ctrl_c, int* mate) {
-  const int M = ctrl_c->M;
+                                              int64_t H, int* mate) {
+  const long long M = H;   // gapped slot space: gap slots have pend = -1
   const long long base = (long long)blockIdx.x * blockDim.x * kMatePerThread + threadIdx.x;
   int e[kMatePerThread], q[kMatePerThread];
 #pragma unroll
@@ -332,7 +332,7 @@ void build_bcsr_mate(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
   // M is on the device (ctrl->M); H bounds it.  pend / outslot were written by the merge.
   const int64_t per_block = (int64_t)T * kMatePerThread;
-  if (a.H > 0) { k_mate<<<(unsigned)((a.H + per_block - 1) / per_block), T, 0, st>>>(a.pend, a.outslot, a.ctrl, a.mate); note_launch(); }
+  if (a.H > 0) { k_mate<<<(unsigned)((a.H + per_block - 1) / per_block), T, 0, st>>>(a.pend, a.outslot, a.H, a.mate); note_launch(); }
 }
 
 void k_ro_to_i32_ext(const int64_t* ro, int64_t n, int* out, int num_sms, cudaStream_t st) {

@@ -158,7 +158,7 @@ struct Layout {
   int32_t layout;
   size_t ctrl, inst_s, inst_t, inst_flow, inst_cut, vbase;
   size_t in_row, in_col, in_cap;           // staging copy of a host CSR
-  size_t h, e, term, deact, deg, cursor, off, soff, roff, rsoff, h1;
+  size_t h, e, term, deact, deg, cursor, off, soff, roff, rsoff, h1, seg;
   size_t q0, q1, hq0, hq1, hc0, hc1, hist, hs;
   size_t scan_part;
   size_t regA, regB, regC;                 // build / residual regions
@@ -185,6 +185,7 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout, int32
   L.h = take(4 * n); L.e = take(8 * n); L.term = take(n); L.deact = take(n); L.h1 = take(4 * n);
   L.deg = take(4 * n + 4); L.cursor = take(4 * n + 4);
   L.off = take(4 * (n + 1)); L.soff = take(4 * (n + 1)); L.roff = take(4 * (n + 1)); L.rsoff = take(4 * (n + 1));
+  L.seg = take(8 * n + 8);   // BCSR: {begin, end} of every vertex segment (gapped layout)
   L.q0 = take(4 * n + 4); L.q1 = take(4 * n + 4);
   int64_t hub = H / kChunk + 64 * (k + 1);   // per-group slices (+64 slack each)
   L.hq0 = take(sizeof(HugeRec) * hub); L.hq1 = take(sizeof(HugeRec) * hub);
@@ -211,7 +212,8 @@ struct SolveParams {
   int k;                 // instances
   int layout;
   int M, Mf;             // slots (BCSR) / forward arcs (RCSR)
-  const int* off;        // BCSR offsets or RCSR forward offsets
+  const int* off;        // RCSR forward offsets
+  const int2* seg;       // BCSR {begin, end} per vertex (segments may be followed by gaps)
   int2* arc;             // {col, cf}
   const int* mate;       // BCSR
   const int* roff;       // RCSR reverse offsets

@@ -51,6 +51,7 @@ struct BuildArgs {
   int* ine;              // BCSR build: input-edge index of every in-list entry (region A + 4m)
   int* pend;             // BCSR build: per slot, an in-half-arc's edge index or -1 (region A + 8m)
   int* outslot;          // BCSR build: per out-half-arc (sorted row position), its merged slot (region D)
+  int2* seg;             // BCSR: {begin, end} of every vertex segment
   int* rsoff;            // BCSR merge build: in-list offsets
   uint8_t* need;         // BCSR merge build: per-row "not sorted" flags
   int* q1;

@@ -112,8 +112,8 @@ struct MergeArgs {
   const int* ioff;          // in-list offsets, n+1
   const uint32_t* ink;      // sorted in-list source ids
   int n;
-  int* mdeg;                // pass 0 output: distinct columns per vertex
-  const int* off;           // pass 1 input: final offsets
+  int* mdeg;                // chunk class: distinct columns per vertex (pass 0)
+  int2* seg;                // pass 1 output: {begin, end} of every vertex segment
   int2* arc;                // pass 1 output
   int* cap0;
   int* outslot;             // pass 1 output: slot of every out-half-arc (by sorted row position)
@@ -131,9 +131,12 @@ __device__ __forceinline__ void emit(const MergeArgs& a, int slot, uint32_t c, l
   a.cap0[slot] = (int)sum;
 }
 
+// PASS 0: classification only (warp-class list, chunk tasks); PASS 1: merge of the
+// thread class (<= kMergeThreadMax elements, one thread per vertex)
 template <int PASS>
 __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
   const int lane = lane_id();
+  long long msum = 0;   // slots written by this thread (ctrl->M)
   for (int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < a.n; base += gridDim.x * blockDim.x) {
     int x = base + lane;
     int ob = 0, lo = 0, ib = 0, li = 0;
@@ -157,9 +160,11 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
         a.mdeg[x] = 0;
       }
     }
-    if (x >= a.n || big) continue;
+    if (PASS == 0 || x >= a.n || big) continue;
+    // gapped layout: seg(x) starts at ooff[x] + ioff[x] (the sum of both list lengths
+    // before x bounds the distinct columns before x), so no counting pass is needed
     int i = 0, j = 0, r = 0;
-    int slot0 = PASS == 1 ? __ldg(a.off + x) : 0;
+    const int slot0 = ob + ib;
     // two-pointer merge; each element is loaded once, the next head of a list is loaded as
     // soon as its current one is consumed (one dependent load per consumed element)
     uint64_t ka = lo > 0 ? a.outk[ob] : kSentKey;
@@ -187,7 +192,12 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
       if (PASS == 1) { emit(a, slot0 + r, c, sum); a.pend[slot0 + r] = e_in; }
       ++r;
     }
-    if (PASS == 0) a.mdeg[x] = r;
+    a.seg[x] = make_int2(slot0, slot0 + r);
+    msum += r;
+  }
+  if (PASS == 1) {
+    msum = warp_sum(msum);
+    if (lane == 0 && msum) atomicAdd(&a.ctrl->M, (int)msum);
   }
 }
 
@@ -257,7 +267,6 @@ __device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int 
   return heads;
 }
 
-template <int PASS>
 __global__ void __launch_bounds__(256) k_merge_warp(MergeArgs a) {
   const int cnt = a.ctrl->mlist_w;
   const int lane = lane_id();
@@ -267,9 +276,9 @@ __global__ void __launch_bounds__(256) k_merge_warp(MergeArgs a) {
     int x = a.wlist[it];
     int ob = __ldg(a.ooff + x), lo = __ldg(a.ooff + x + 1) - ob;
     int ib = __ldg(a.ioff + x), li = __ldg(a.ioff + x + 1) - ib;
-    int base = PASS == 1 ? __ldg(a.off + x) : 0;
-    int h = warp_merge_range<PASS>(a, ob, lo, ib, li, 0, 0, 0, lo + li, kInf, base);
-    if (PASS == 0 && lane == 0) a.mdeg[x] = h;
+    const int base = ob + ib;   // gapped layout (see k_merge_thread)
+    int h = warp_merge_range<1>(a, ob, lo, ib, li, 0, 0, 0, lo + li, kInf, base);
+    if (lane == 0) { a.seg[x] = make_int2(base, base + h); atomicAdd(&a.ctrl->M, h); }
   }
 }
 
@@ -317,7 +326,13 @@ __global__ void __launch_bounds__(256) k_merge_chunk(MergeArgs a) {
       int before = 0;
       for (int q = lane; q < c; q += 32) before += a.chunk_heads[t - c + q];
       before = warp_sum(before);
-      warp_merge_range<1>(a, ob, lo, ib, li, i0, j0, k0, k1, prev, __ldg(a.off + x) + before);
+      const int base = ob + ib;   // gapped layout (see k_merge_thread)
+      warp_merge_range<1>(a, ob, lo, ib, li, i0, j0, k0, k1, prev, base + before);
+      if (c == 0 && lane == 0) {
+        const int d = __ldg(a.mdeg + x);
+        a.seg[x] = make_int2(base, base + d);
+        atomicAdd(&a.ctrl->M, d);
+      }
     }
   }
 }
@@ -366,18 +381,15 @@ void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
   cudaMemsetAsync(a.pend, 0xff, sizeof(int) * a.H, st);   // (src is dead: pend reuses its space)
   MergeArgs ma;
   ma.ooff = a.soff; ma.outk = outk; ma.ioff = a.rsoff; ma.ink = ink; ma.n = (int)n;
-  ma.mdeg = a.deg; ma.off = a.off; ma.arc = a.arc; ma.cap0 = a.cap0;
+  ma.mdeg = a.deg; ma.seg = a.seg; ma.arc = a.arc; ma.cap0 = a.cap0;
   ma.outslot = a.outslot; ma.pend = a.pend; ma.ine = a.ine;
   ma.wlist = a.q0; ma.tasks = a.mtasks; ma.chunk_heads = a.mheads; ma.ctrl = a.ctrl;
   cudaMemsetAsync(&a.ctrl->mlist_w, 0, 2 * sizeof(int), st);
-  { k_merge_thread<0><<<gridcap(n, T, a.num_sms, 16), T, 0, st>>>(ma); note_launch(); }
-  { k_merge_warp<0><<<a.num_sms * 16, T, 0, st>>>(ma); note_launch(); }
-  { k_merge_chunk<0><<<a.num_sms * 4, T, 0, st>>>(ma); note_launch(); }
-  cudaMemcpyAsync(a.off, a.deg, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
-  exclusive_scan(a.off, n, a.scan_part, st);
-  cudaMemcpyAsync(&a.ctrl->M, a.off + n, sizeof(int), cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(&a.ctrl->M, 0, sizeof(int), st);
+  { k_merge_thread<0><<<gridcap(n, T, a.num_sms, 16), T, 0, st>>>(ma); note_launch(); }   // classify
+  { k_merge_chunk<0><<<a.num_sms * 4, T, 0, st>>>(ma); note_launch(); }                  // hub chunk counts
   { k_merge_thread<1><<<gridcap(n, T, a.num_sms, 16), T, 0, st>>>(ma); note_launch(); }
-  { k_merge_warp<1><<<a.num_sms * 16, T, 0, st>>>(ma); note_launch(); }
+  { k_merge_warp<<<a.num_sms * 16, T, 0, st>>>(ma); note_launch(); }
   { k_merge_chunk<1><<<a.num_sms * 4, T, 0, st>>>(ma); note_launch(); }
 }
 

@@ -45,11 +45,11 @@ struct Seg {
 };
 
 struct BcsrOps {
-  const int* off; int2* arc; const int* mate;
+  const int2* segs; int2* arc; const int* mate;   // segs[u] = {begin, end} (gapped layout)
   unsigned long long pf = 0;   // L2 evict_first policy for streamed arrays
   __device__ void init() { pf = policy_evict_first(); }
-  __device__ Seg seg(int u) const { Seg s; s.fb = __ldg(off + u); s.fe = __ldg(off + u + 1); s.rb = s.re = 0; return s; }
-  __device__ int degree(int u) const { return __ldg(off + u + 1) - __ldg(off + u); }
+  __device__ Seg seg(int u) const { const int2 b = __ldg(segs + u); Seg s; s.fb = b.x; s.fe = b.y; s.rb = s.re = 0; return s; }
+  __device__ int degree(int u) const { const int2 b = __ldg(segs + u); return b.y - b.x; }
   // residual out-arc #i of u: u -> col with residual capacity cf, identified by slot
   __device__ void out_arc(const Seg& s, int i, int& col, int& cf, int& slot) const {
     slot = s.fb + i;
@@ -147,7 +147,10 @@ constexpr int kSmallMax = 512;    // small-frontier mode: queues up to this size
 constexpr int kSmallDeg = 8;      // small-frontier mode: largest degree processed by one thread
 constexpr int kSB = 4;            // small-frontier mode: slots loaded per batch (independent loads)
 constexpr int kGapBins = 256;     // online gap: shared-memory bins for the lowest levels
-constexpr int kBuThread = 32;     // bottom-up BFS: vertices up to this many slots are scanned by one thread
+#ifndef WBPR_BUT
+#define WBPR_BUT 32
+#endif
+constexpr int kBuThread = WBPR_BUT; // bottom-up BFS: vertices up to this many slots are scanned by one thread
 constexpr int kBuB = 8;           // bottom-up BFS: slots loaded per batch (independent loads)
 constexpr int kTdThread = 8;      // top-down BFS: frontier vertices up to this many slots are scanned by one thread
 constexpr int kTdPack = 4;        // top-down BFS: pack 32 frontier entries per warp when |frontier| >= kTdPack x warps
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
   HugeRec* const HQ[2] = {P.hq[0] + GD.hub0, P.hq[1] + GD.hub0};
   int2* const HC[2] = {P.hc[0] + 2 * GD.hub0, P.hc[1] + 2 * GD.hub0};
   int2* const HS = P.hs + 2 * GD.hub0;
-  const int Mslots = P.layout == 0 ? (__ldg(P.off + VHI) - __ldg(P.off + VLO))
+  const int Mslots = P.layout == 0 ? (__ldg(&P.seg[VHI - 1].y) - __ldg(&P.seg[VLO].x))
                                    : 2 * (__ldg(P.off + VHI) - __ldg(P.off + VLO));
   const unsigned long long gr_threshold =
       (unsigned long long)((double)P.gr_beta * (double)((long long)(VHI - VLO) + (long long)Mslots)) + 1;
@@ -890,8 +893,9 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             int dself = 0;
             Seg sv;
             sv.fb = sv.fe = sv.rb = sv.re = 0;
-            if (hv == N) { sv = ops.seg(v); dself = sv.deg(); }
-            const bool thr = hv == N && dself <= kBuThread;
+            const bool unl = hv == N && !(phase == 1 && ld_term(P.deact + v));   // frozen: never reachable
+            if (unl) { sv = ops.seg(v); dself = sv.deg(); }
+            const bool thr = unl && dself <= kBuThread;
             if (thr) {
               int scanned = 0;
               for (int b0 = 0; b0 < dself && !self_hit; b0 += kBuB) {
@@ -911,7 +915,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               st_bfs_arcs += scanned;   // per-thread partial; summed over the block at the end
               if (self_hit) st_cg(P.h + v, level + 1);
             }
-            unsigned todo = __ballot_sync(FULL, hv == N && !thr);
+            unsigned todo = __ballot_sync(FULL, unl && !thr);
             unsigned found_mask = __ballot_sync(FULL, self_hit);
             while (todo) {
               int j = __ffs(todo) - 1;
@@ -941,7 +945,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           for (int t = gwarp; t < nhs; t += nwarps) {
             int2 hsk = ld_cg(HS + t);
             int vv = hsk.x;
-            if (ld_cg_hint(P.h + vv, pl) != N) continue;
+            if (ld_cg_hint(P.h + vv, pl) != N || (phase == 1 && ld_term(P.deact + vv))) continue;
             Seg sg = ops.seg(vv);
             int lo2 = hsk.y * kChunk, hi2 = min(sg.deg(), lo2 + kChunk);
             int scanned = 0;
@@ -987,18 +991,21 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             if (hv0 < kGapBins) atomicAdd(&S.gbin[hv0], 1);
             else if (hv0 < N) atomicAdd(P.hist + hv0, 1);
           }
-          if (v < VHI) {
-            long long ev = ld_cg(P.e + v);
-            if (ev > 0 && ld_term(P.term + v) == 0) {
-              int hv = ld_cg(P.h + v);
-              if (hv < N) {
+          if (v < VHI && ld_term(P.term + v) == 0) {
+            const int hv = ld_cg(P.h + v);
+            const long long ev = ld_cg(P.e + v);
+            if (hv < N) {
+              if (ev > 0) {
                 act = true;
                 dg = ops.degree(v);
                 huge = dg > kChunk;
-              } else if (phase == 1 && !P.deact[v]) {
-                P.deact[v] = 1;
-                dropped += (unsigned long long)ev;
               }
+            } else if (phase == 1 && !ld_term(P.deact + v)) {
+              // v cannot reach a sink: it stays so for the rest of phase 1 (the set is closed,
+              // §8(c) N5) - frozen: its excess leaves Excess_total once and later
+              // bottom-up BFS levels skip it
+              P.deact[v] = 1;
+              if (ev > 0) dropped += (unsigned long long)ev;
             }
           }
           if (lane == 0) st_cand += min(32, VHI - base);
@@ -1342,7 +1349,7 @@ int solve_max_blocks_per_sm(int layout, int threads) {
 cudaError_t launch_solve(const SolveParams& p, int blocks, int threads, cudaStream_t st) {
   note_launch();
   if (p.layout == 0) {
-    BcsrOps o{p.off, p.arc, p.mate};
+    BcsrOps o{p.seg, p.arc, p.mate};
     void* args[] = {(void*)&p, (void*)&o};
     return cudaLaunchCooperativeKernel(solve_fn<BcsrOps>(), dim3(blocks), dim3(threads), args, 0, st);
   } else {

@@ -68,7 +68,7 @@ class Stats(ctypes.Structure):
 
 class Residual(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int32), ("n", ctypes.c_int64), ("M", ctypes.c_int64), ("Mf", ctypes.c_int64)] + [
-        (name, ctypes.c_void_p) for name in ("off", "arc", "mate", "cap0", "roff", "rarc", "bcf", "e", "h")]
+        (name, ctypes.c_void_p) for name in ("off", "arc", "mate", "cap0", "roff", "rarc", "bcf", "e", "h", "seg")]
 
 
 _lib = None
@@ -303,9 +303,9 @@ def residual(workspace: Workspace) -> dict:
 
     n = v.n
     out = dict(layout=v.layout, n=n, M=v.M, Mf=v.Mf)
-    if v.layout == 0:
+    if v.layout == 0:   # gapped: vertex u owns slots [seg[u, 0], seg[u, 1]) of the M-slot space
         arc = grab(v.arc, 2 * v.M, torch.int32).reshape(-1, 2)
-        out.update(off=grab(v.off, n + 1, torch.int32), col=arc[:, 0].copy(), cf=arc[:, 1].copy(),
+        out.update(seg=grab(v.seg, 2 * n, torch.int32).reshape(-1, 2), col=arc[:, 0].copy(), cf=arc[:, 1].copy(),
                    mate=grab(v.mate, v.M, torch.int32), cap0=grab(v.cap0, v.M, torch.int32))
     else:
         farc = grab(v.arc, 2 * v.Mf, torch.int32).reshape(-1, 2)

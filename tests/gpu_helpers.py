@@ -22,6 +22,28 @@ def gpu_solve(g, layout="bcsr", ws=None, **opt):
     return F, bm.cpu().numpy().view(np.uint32), st, ws
 
 
+def dense_bcsr(R):
+    """The gapped BCSR view (segments [seg[u,0], seg[u,1]) in vertex order, unused slots
+    between them) compacted to the dense layout of oracle/residual_ref.bcsr: off, col, cf,
+    cap0 and mate re-indexed to dense slots.  Also checks the gap invariants."""
+    seg = R["seg"].astype(np.int64)
+    b, e = seg[:, 0], seg[:, 1]
+    lens = e - b
+    assert np.all(lens >= 0)
+    assert np.all(b[1:] >= e[:-1]), "segments overlap or are out of vertex order"
+    n = seg.shape[0]
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    M = int(off[-1])
+    shift = b - off[:-1]                       # gapped slot = dense slot + shift[owner]
+    idx = np.repeat(shift, lens) + np.arange(M, dtype=np.int64)
+    col = R["col"][idx]
+    gm = R["mate"][idx].astype(np.int64)
+    mate = gm - shift[col]                     # the reverse arc lives in seg(col)
+    return dict(M=M, off=off.astype(np.int32), col=col.copy(), cf=R["cf"][idx].copy(),
+                cap0=R["cap0"][idx].copy(), mate=mate.astype(np.int32))
+
+
 def bits_to_mask(words, n):
     b = np.unpackbits(np.asarray(words, np.uint32).view(np.uint8), bitorder="little")
     return b[:n].astype(np.uint8)
@@ -42,7 +64,8 @@ def assert_parity(g, layout="bcsr", ref=None, validate=True, **opt):
     if validate:
         R = W.residual(ws)
         if layout == "bcsr":
-            f = check.demerge_bcsr(g.n, g.row_off, g.col, g.cap, R["off"], R["col"], R["cf"], R["cap0"], R["mate"])
+            D = dense_bcsr(R)
+            f = check.demerge_bcsr(g.n, g.row_off, g.col, g.cap, D["off"], D["col"], D["cf"], D["cap0"], D["mate"])
         else:
             f = check.demerge_rcsr(g.n, g.row_off, g.col, g.cap, R["foff"], R["fcol"], R["fcf"], R["cap0"], R["bcf"])
         check.check_flow(g.n, g.row_off, g.col, g.cap, g.s, g.t, F, bits_to_mask(words, g.n), f,

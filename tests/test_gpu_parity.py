@@ -8,7 +8,7 @@ import pytest
 import oracle
 import synth
 from oracle import brute, matching, residual_ref
-from tests.gpu_helpers import assert_parity, bits_to_mask, gpu_solve, to_dev
+from tests.gpu_helpers import assert_parity, bits_to_mask, dense_bcsr, gpu_solve, to_dev
 
 pytestmark = pytest.mark.gpu
 LAYOUTS = ["bcsr", "rcsr"]
@@ -66,9 +66,10 @@ def _build_graph(kind, seed):
 @pytest.mark.parametrize("kind,seed", BUILD_CASES)
 def test_build_bcsr_bitexact(kind, seed):
     g = _build_graph(kind, seed)
-    R, st = _build(g, "bcsr")
+    G, st = _build(g, "bcsr")
+    R = dense_bcsr(G)
     ref = residual_ref.bcsr(g.n, g.row_off, g.col, g.cap)
-    assert R["M"] == ref["col"].shape[0]
+    assert R["M"] == ref["col"].shape[0] == st["M"]
     assert np.array_equal(R["off"], ref["off"])
     assert np.array_equal(R["col"], ref["col"])
     assert np.array_equal(R["cf"], ref["cf0"])

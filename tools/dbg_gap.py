@@ -3,7 +3,7 @@ sys.path.insert(0, os.getcwd())
 import numpy as np, torch, synth, oracle
 import paper_2404_00270_b200 as W
 from oracle import check
-from tests.gpu_helpers import to_dev
+from tests.gpu_helpers import dense_bcsr, to_dev
 g = synth.grid(40, 30, True, 2)
 ref = oracle.maxflow_graph(g, phase2=False)
 ro, col, cap = to_dev(g)
@@ -13,7 +13,8 @@ try:
     print("ok", F)
 except Exception as e:
     print("ERR", e)
-R = W.residual(ws)
+R0 = W.residual(ws)
+R = dict(R0, **dense_bcsr(R0))
 N = g.n
 e = R["e"]; h = R["h"]
 print("e(t)", e[g.t], "ref", ref.flow, "sum e", e.sum(), "neg e", (e < 0).sum(), "neg cf", (R["cf"] < 0).sum())
