@@ -126,7 +126,7 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
   a.mheads = at<int>(W.base, L.hc1);
   a.ine = at<int>(W.base, L.regA + 4 * (size_t)L.m);
   a.src = at<int>(W.base, L.regA + 8 * (size_t)L.m);
-  a.pend = at<int>(W.base, L.regA + 8 * (size_t)L.m);
+  a.inslot = at<int>(W.base, L.regA + 8 * (size_t)L.m);
   a.outslot = at<int>(W.base, L.regD);
   a.seg = at<int2>(W.base, L.seg);
 

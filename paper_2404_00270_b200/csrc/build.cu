@@ -218,22 +218,24 @@ __global__ void k_colcopy(const int2* __restrict__ arc, const Ctrl* ctrl, int* c
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < M; p += gridDim.x * blockDim.x) colv[p] = arc[p].x;
 }
 
-// mate[] from the edge identities carried through the construction (merge.cu): every
-// slot q that received an in-half-arc of input edge e = (u -> x) pairs with the slot
-// outslot[e] of e's out-half-arc in seg(u) — the paper's backward-arc binary search
-// replaced by one lookup per pair.  Pairs with arcs in both directions are
-// written from both sides (same values); every slot is written by itself or its partner.
+// mate[] from the edge identities carried through the construction (merge.cu): the
+// in-list entry t of input edge e = ine[t] = (u -> x) sits at slot q = inslot[t] of seg(x)
+// and pairs with the slot p = outslot[e] of e's out-half-arc in seg(u) — the paper's
+// backward-arc binary search replaced by one lookup per input edge.  Pairs
+// with arcs in both directions (and parallel edges) are written more than once, always
+// with the same values; every slot is written by itself or by its partner.
 constexpr int kMatePerThread = 4;
-__global__ void __launch_bounds__(256) k_mate(const int* __restrict__ pend, const int* __restrict__ outslot,
-                                              int64_t H, int* mate) {
-  const long long M = H;   // gapped slot space: gap slots have pend = -1
-  const long long base = (long long)blockIdx.x * blockDim.x * kMatePerThread + threadIdx.x;
+__global__ void __launch_bounds__(256) k_mate(const int* __restrict__ ine, const int* __restrict__ inslot,
+                                              const int* __restrict__ outslot, const int* __restrict__ rsoff, int n,
+                                              int* mate) {
+  const int total = __ldg(rsoff + n);   // in-list entries
+  const int base = blockIdx.x * blockDim.x * kMatePerThread + threadIdx.x;
   int e[kMatePerThread], q[kMatePerThread];
 #pragma unroll
   for (int r = 0; r < kMatePerThread; ++r) {
-    const long long qq = base + (long long)r * blockDim.x;
-    q[r] = qq < M ? (int)qq : -1;
-    e[r] = q[r] >= 0 ? __ldg(pend + q[r]) : -1;
+    const int t = base + r * blockDim.x;
+    e[r] = t < total ? __ldg(ine + t) : -1;
+    q[r] = t < total ? __ldg(inslot + t) : -1;
   }
   int p[kMatePerThread];
 #pragma unroll
@@ -330,9 +332,9 @@ void build_bcsr(const BuildArgs& a, cudaStream_t st) {
 
 void build_bcsr_mate(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
-  // M is on the device (ctrl->M); H bounds it.  pend / outslot were written by the merge.
+  // one thread per kMatePerThread in-list entries (rsoff[n] of them; m bounds it)
   const int64_t per_block = (int64_t)T * kMatePerThread;
-  if (a.H > 0) { k_mate<<<(unsigned)((a.H + per_block - 1) / per_block), T, 0, st>>>(a.pend, a.outslot, a.H, a.mate); note_launch(); }
+  if (a.m > 0) { k_mate<<<(unsigned)((a.m + per_block - 1) / per_block), T, 0, st>>>(a.ine, a.inslot, a.outslot, a.rsoff, (int)a.n, a.mate); note_launch(); }
 }
 
 void k_ro_to_i32_ext(const int64_t* ro, int64_t n, int* out, int num_sms, cudaStream_t st) {

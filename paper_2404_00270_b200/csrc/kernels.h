@@ -49,7 +49,7 @@ struct BuildArgs {
   int k;
   int* src;              // BCSR build: owner row of every input edge (region A + 8m; dead after the in-list resolve)
   int* ine;              // BCSR build: input-edge index of every in-list entry (region A + 4m)
-  int* pend;             // BCSR build: per slot, an in-half-arc's edge index or -1 (region A + 8m)
+  int* inslot;           // BCSR build: merged slot of every in-list entry (region A + 8m; src is dead by then)
   int* outslot;          // BCSR build: per out-half-arc (sorted row position), its merged slot (region D)
   int2* seg;             // BCSR: {begin, end} of every vertex segment
   int* rsoff;            // BCSR merge build: in-list offsets

@@ -117,8 +117,7 @@ struct MergeArgs {
   int2* arc;                // pass 1 output
   int* cap0;
   int* outslot;             // pass 1 output: slot of every out-half-arc (by sorted row position)
-  int* pend;                // pass 1 output: per slot, the edge index of one of its in-half-arcs (else -1)
-  const int* ine;           // edge index of every in-list entry
+  int* inslot;              // pass 1 output: slot of every in-list entry (by in-list position)
   int* wlist;               // vertices for the warp class
   int2* tasks;              // (vertex, chunk) tasks of the chunked class (> kMergeWarpMax)
   int* chunk_heads;         // distinct columns found by each chunk task
@@ -169,7 +168,6 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
     // soon as its current one is consumed (one dependent load per consumed element)
     uint64_t ka = lo > 0 ? a.outk[ob] : kSentKey;
     uint32_t kb = li > 0 ? a.ink[ib] : kInf;
-    int eb = (PASS == 1 && li > 0) ? a.ine[ib] : 0;
     while (true) {
       uint32_t ca = kcol(ka);
       const uint32_t c = ca < kb ? ca : kb;
@@ -182,14 +180,12 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
         ka = i < lo ? a.outk[ob + i] : kSentKey;
         ca = kcol(ka);
       }
-      int e_in = -1;
       while (kb == c) {
-        if (e_in < 0) e_in = eb;
+        if (PASS == 1) a.inslot[ib + j] = slot0 + r;
         ++j;
         kb = j < li ? a.ink[ib + j] : kInf;
-        if (PASS == 1) eb = j < li ? a.ine[ib + j] : 0;
       }
-      if (PASS == 1) { emit(a, slot0 + r, c, sum); a.pend[slot0 + r] = e_in; }
+      if (PASS == 1) emit(a, slot0 + r, c, sum);
       ++r;
     }
     a.seg[x] = make_int2(slot0, slot0 + r);
@@ -245,7 +241,7 @@ __device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int 
       // head in this window continues the previous window's last slot)
       const int slot = slot_base + heads + __popc(hm & (((1u << lane) - 1u) | (1u << lane))) - 1;
       if (takeA) a.outslot[ob + i0 + i] = slot;
-      else a.pend[slot] = a.ine[ib + j0 + j];   // any in-half-arc of the run (parallel edges share the slot)
+      else a.inslot[ib + j0 + j] = slot;
     }
     if (PASS == 1 && head) {
       long long sum = 0;
@@ -378,11 +374,10 @@ void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
   }
   segmented_sort32(ink, itmp, a.rsoff, (int)n, a.maxlen, a.ctrl, items, items_med, a.q0, a.num_sms, st);
   if (m > 0) { k_in_resolve<<<(unsigned)((m + 1023) / 1024), T, 0, st>>>(ink, a.ine, a.src, a.rsoff, (int)n); note_launch(); }
-  cudaMemsetAsync(a.pend, 0xff, sizeof(int) * a.H, st);   // (src is dead: pend reuses its space)
   MergeArgs ma;
   ma.ooff = a.soff; ma.outk = outk; ma.ioff = a.rsoff; ma.ink = ink; ma.n = (int)n;
   ma.mdeg = a.deg; ma.seg = a.seg; ma.arc = a.arc; ma.cap0 = a.cap0;
-  ma.outslot = a.outslot; ma.pend = a.pend; ma.ine = a.ine;
+  ma.outslot = a.outslot; ma.inslot = a.inslot;
   ma.wlist = a.q0; ma.tasks = a.mtasks; ma.chunk_heads = a.mheads; ma.ctrl = a.ctrl;
   cudaMemsetAsync(&a.ctrl->mlist_w, 0, 2 * sizeof(int), st);
   cudaMemsetAsync(&a.ctrl->M, 0, sizeof(int), st);
