@@ -51,6 +51,14 @@ WBPR_DEV int2 ld_cg_hint(const int2* p, unsigned long long pol) {
 WBPR_DEV int ld_cg_hint(const int* p, unsigned long long pol) {
   int v; asm volatile("ld.global.cg.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
 }
+// L1-allocating load with an L2 hint, for gathers of neighbour labels h[v] (a few hot
+// vertices are read by many warps of an SM).  L1 is not coherent across SMs, but every
+// grid barrier of the solve kernel ends with an acquire (CCTL.IVALL invalidates the SM's
+// L1), so a cached label is never older than the current phase; inside a phase a stale
+// label is one of the interleavings the lock-free algorithm already admits.
+WBPR_DEV int ld_ca_hint(const int* p, unsigned long long pol) {
+  int v; asm volatile("ld.global.ca.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
+}
 WBPR_DEV int ld_nc_hint(const int* p, unsigned long long pol) {
   int v; asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
 }

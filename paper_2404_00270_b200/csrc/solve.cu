@@ -152,6 +152,13 @@ constexpr int kGapBins = 256;     // online gap: shared-memory bins for the lowe
 #endif
 constexpr int kBuThread = WBPR_BUT; // bottom-up BFS: vertices up to this many slots are scanned by one thread
 constexpr int kBuB = 8;           // bottom-up BFS: slots loaded per batch (independent loads)
+// neighbour-label gathers: L2-only (default) or L1-allocating
+#ifndef WBPR_H_L1
+#define WBPR_H_L1 0   // measured: L1-allocating label gathers gave no gain (B200, C5/C3/C4)
+#endif
+__device__ __forceinline__ int ld_h(const int* p, unsigned long long pol) {
+  return WBPR_H_L1 ? ld_ca_hint(p, pol) : ld_cg_hint(p, pol);
+}
 constexpr int kTdThread = 8;      // top-down BFS: frontier vertices up to this many slots are scanned by one thread
 constexpr int kTdPack = 4;        // top-down BFS: pack 32 frontier entries per warp when |frontier| >= kTdPack x warps
 #ifndef WBPR_RU
@@ -515,7 +522,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       int dgc[kSB];
 #pragma unroll
       for (int j = 0; j < kSB; ++j) {
-        hv[j] = cf[j] > 0 ? ld_cg_hint(P.h + col[j], pl) : INT_MAX;
+        hv[j] = cf[j] > 0 ? ld_h(P.h + col[j], pl) : INT_MAX;
         dgc[j] = (P.push_mode != 0 && cf[j] > 0) ? ops.degree(col[j]) : 0;
       }
 #pragma unroll
@@ -577,7 +584,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         if (b0 + j < d) ops.in_arc(sg, b0 + j, u[j], cf[j]);
       }
 #pragma unroll
-      for (int j = 0; j < kSB; ++j) hu8[j] = cf[j] > 0 ? ld_cg_hint(P.h + u[j], pl) : -1;
+      for (int j = 0; j < kSB; ++j) hu8[j] = cf[j] > 0 ? ld_h(P.h + u[j], pl) : -1;
 #pragma unroll
       for (int j = 0; j < kSB; ++j)
         if (cf[j] > 0 && hu8[j] == N && atomicCAS(P.h + u[j], N, lvl + 1) == N) small_append(u[j], ops.degree(u[j]));
@@ -600,7 +607,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       }
       bool ok = false;
 #pragma unroll
-      for (int j = 0; j < kRU; ++j) ok |= cf[j] > 0 && ld_cg_hint(P.h + col[j], pl) == level;
+      for (int j = 0; j < kRU; ++j) ok |= cf[j] > 0 && ld_h(P.h + col[j], pl) == level;
       scanned += min(32 * kRU, hi - b);
       if (__ballot_sync(FULL, ok)) return true;
     }
@@ -619,7 +626,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         if (i < hi) ops.in_arc(sg, i, u[j], cf[j]);
       }
 #pragma unroll
-      for (int j = 0; j < kRU; ++j) hu[j] = cf[j] > 0 ? ld_cg_hint(P.h + u[j], pl) : -1;
+      for (int j = 0; j < kRU; ++j) hu[j] = cf[j] > 0 ? ld_h(P.h + u[j], pl) : -1;
       bool found[kRU];
 #pragma unroll
       for (int j = 0; j < kRU; ++j)   // sinks 0, sources N+1: never N; level(u) = level(w) + 1
@@ -844,7 +851,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               }
               int hu[kBuB];
 #pragma unroll
-              for (int j = 0; j < kBuB; ++j) hu[j] = cf[j] > 0 ? ld_cg_hint(P.h + u[j], pl) : -1;
+              for (int j = 0; j < kBuB; ++j) hu[j] = cf[j] > 0 ? ld_h(P.h + u[j], pl) : -1;
               bool found[kBuB];
 #pragma unroll
               for (int j = 0; j < kBuB; ++j) found[j] = hu[j] == N && atomicCAS(P.h + u[j], N, level + 1) == N;
@@ -907,7 +914,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
                 }
                 int hl[kBuB];
 #pragma unroll
-                for (int j = 0; j < kBuB; ++j) hl[j] = cf[j] > 0 ? ld_cg_hint(P.h + col[j], pl) : -1;
+                for (int j = 0; j < kBuB; ++j) hl[j] = cf[j] > 0 ? ld_h(P.h + col[j], pl) : -1;
 #pragma unroll
                 for (int j = 0; j < kBuB; ++j) self_hit |= hl[j] == level;
                 scanned += min(kBuB, dself - b0);
@@ -1108,7 +1115,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             int col, cf, slot;
             ops.out_arc(sg, i, col, cf, slot);
             if (cf > 0) {
-              unsigned hv = (unsigned)ld_cg_hint(P.h + col, pl);
+              unsigned hv = (unsigned)ld_h(P.h + col, pl);
               unsigned long long cand = ((unsigned long long)hv << 32) | (unsigned)slot;
               if (cand < best) { best = cand; bcf = cf; bcol = col; }
             }
@@ -1131,7 +1138,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               if (i < hi) ops.out_arc(sg, i, col[j], cf[j], slot[j]);
             }
 #pragma unroll
-            for (int j = 0; j < kRU; ++j) hv[j] = cf[j] > 0 ? ld_cg_hint(P.h + col[j], pl) : INT_MAX;
+            for (int j = 0; j < kRU; ++j) hv[j] = cf[j] > 0 ? ld_h(P.h + col[j], pl) : INT_MAX;
             long long want = 0;            // admissible capacity of the whole super-group
             unsigned amask = 0;            // groups with an admissible arc
 #pragma unroll
