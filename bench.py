@@ -50,6 +50,11 @@ def log(*a):
 
 
 # ---------------------------------------------------------------------------- workloads
+# Solver options the bench uses per workload unless --opt overrides them (wbpr_options
+# fields).  C5: a global relabel after 0.5x (instead of 1x) the last GR's
+# time in rounds - measured best on C5 (γ sweep in profiles/r1/); results are exact for
+# every γ, it only moves time between rounds and global relabels.
+WORKLOAD_OPTS = {"c5": {"gr_gamma": 0.5}}
 def make_workload(name, rank, world):
     """Returns dict(kind, parts|graph, ids, desc) for this rank."""
     import synth
@@ -61,6 +66,12 @@ def make_workload(name, rank, world):
         return dict(kind="batch", parts=parts, ids=list(range(lo, hi)), total=total,
                     desc="C5: 64 x R-MAT scale 18 (edgefactor 16, U[1,100] caps, 20 paper-rule s/t pairs "
                          "behind super terminals), seeds 1000-1063, partitioned over ranks")
+    if name == "c4":
+        nL = nR = 1 << 20
+        l, r = synth.bipartite_edges(nL, nR, 1 << 24, 1)
+        return dict(kind="bipartite", nL=nL, nR=nR, l=l, r=r, ids=[rank], total=1,
+                    desc="C4: bipartite matching 2^20 x 2^20, 2^24 uniform draws (duplicates collapsed), unit "
+                         "capacities via super source/sink (network built on the device, A9)")
     g = {"c1": lambda: synth.random_graph(1024, 8192, 1),
          "c2": lambda: synth.grid(1024, 1024, False, 1),
          "c2r": lambda: synth.grid(1024, 1024, True, 1),
@@ -164,6 +175,8 @@ def run_wbpr(args, rank, world, local_rank):
     t0 = time.time()
     wl = make_workload(args.workload, rank, world)
     gen_s = time.time() - t0
+    if wl["kind"] == "bipartite":
+        return run_bipartite(args, rank, world, dev, wl, gen_s)
     if wl["kind"] == "batch":
         B = union_of(wl["parts"])
         G = B.union
@@ -178,7 +191,7 @@ def run_wbpr(args, rank, world, local_rank):
     ro_h = torch.from_numpy(G.row_off).pin_memory()
     col_h = torch.from_numpy(G.col).pin_memory()
     cap_h = torch.from_numpy(G.cap).pin_memory()
-    opt = dict(layout=args.layout)
+    opt = dict(layout=args.layout, **WORKLOAD_OPTS.get(args.workload, {}))
     for kv in args.opt:
         k_, v_ = kv.split("=")
         opt[k_] = float(v_) if "." in v_ else int(v_)
@@ -283,7 +296,8 @@ def run_wbpr(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "int64",
         "data": "synthetic",
-        "config": {"workload": args.workload, "desc": wl["desc"], "layout": args.layout, "options": args.opt,
+        "config": {"workload": args.workload, "desc": wl["desc"], "layout": args.layout,
+                   "options": {k_: v_ for k_, v_ in opt.items() if k_ != "layout"},
                    "instances_per_rank": k, "n_per_rank": int(G.n), "m_per_rank": int(G.m),
                    "parallelism": f"instances sharded over {world} rank(s); NCCL all_gather of 64-B records",
                    "l2": "inputs and workspace larger than L2 (126 MB)"},
@@ -310,9 +324,122 @@ def run_wbpr(args, rank, world, local_rank):
     return out
 
 
+def run_bipartite(args, rank, world, dev, wl, gen_s):
+    """C4 (A9): maximum bipartite matching through wbpr_bipartite_match (network built on
+    the device).  value = matchings/s of the whole job (weak scaling: one instance per rank)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2404_00270_b200 as W
+    nL, nR = wl["nL"], wl["nR"]
+    l_h = torch.from_numpy(wl["l"]).pin_memory()
+    r_h = torch.from_numpy(wl["r"]).pin_memory()
+    l_d, r_d = l_h.to(dev), r_h.to(dev)
+    match_h = torch.empty(nL, dtype=torch.int32).pin_memory()
+    opt = dict(layout=args.layout, **WORKLOAD_OPTS.get(args.workload, {}))
+    for kv in args.opt:
+        k_, v_ = kv.split("=")
+        opt[k_] = float(v_) if "." in v_ else int(v_)
+    ws = W.Workspace(1 << 20, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(host=False):
+        if host:   # e2e: inputs H2D from pinned memory and the matching D2H inside the timed region
+            l_d.copy_(l_h, non_blocking=True)
+            r_d.copy_(r_h, non_blocking=True)
+        size, match, st = W.bipartite_match(nL, nR, l_d, r_d, workspace=ws, **opt)
+        if host:
+            match_h.copy_(match, non_blocking=True)
+        return size, match, st
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk = ClockSampler(dev.index)
+    clk.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sts = []
+    ev0.record(stream)
+    for _ in range(args.steps):
+        size, match, st = step()
+        sts.append(st)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    e2e_steps = max(1, min(args.steps, 5))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        step(host=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1)
+    times = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(times[0]), float(times[1])
+    if rank != 0:
+        return None
+    assert size == sts[-1]["flow_value"] == sts[-1]["cut_capacity"]
+    hbm, peak_src = peaks()
+    solve_ms = float(np.mean([x["solve_ms"] for x in sts]))
+    build_ms = float(np.mean([x["build_ms"] for x in sts]))
+    total_ms = float(np.mean([x["total_ms"] for x in sts]))
+    st = sts[-1]
+    sb = solve_bytes(st)
+    achieved = sb / (solve_ms / 1e3) / 1e9
+    gteps = (st["arcs_scanned"] + st["bfs_arcs_scanned"]) / (solve_ms / 1e3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(world * args.steps / (ms / 1e3), 3), "unit": "matchings/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": "c4", "desc": wl["desc"], "layout": args.layout,
+                   "options": {k_: v_ for k_, v_ in opt.items() if k_ != "layout"}, "nL": nL, "nR": nR,
+                   "edges": int(wl["l"].shape[0]), "parallelism": f"replicas ({world} rank(s), one instance each)",
+                   "l2": "inputs and workspace larger than L2 (126 MB)"},
+        "per_step": {"total_ms": round(total_ms, 3), "build_ms": round(build_ms, 3), "solve_ms": round(solve_ms, 3),
+                     "rounds": st["rounds"], "global_relabels": st["global_relabels"], "bfs_levels": st["bfs_levels"],
+                     "pushes": st["pushes"], "relabels": st["relabels"], "arcs_scanned": st["arcs_scanned"],
+                     "bfs_arcs_scanned": st["bfs_arcs_scanned"], "residual_gteps": round(gteps, 3), "M": st["M"],
+                     "matching_size": int(size)},
+        "roofline": {"bound": "hbm", "kernel": "k_solve (persistent push-relabel + device GR, 1 launch/step)",
+                     "achieved": round(achieved, 2), "peak": hbm, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "algorithmic_bytes_per_launch": int(sb),
+                     "launch_ms": round(solve_ms, 3), "traffic": None},
+        "e2e": {"value": round(world * e2e_steps / (e2e_ms / 1e3), 3), "unit": "matchings/s",
+                "h2d_bytes_per_step": int(wl["l"].nbytes + wl["r"].nbytes), "d2h_bytes_per_step": 4 * nL,
+                "steps": e2e_steps},
+        "gpu_launches": int(st["kernel_launches"]) * args.steps,
+        "clocks": clocks,
+        "gen_s": round(gen_s, 2),
+    }
+    if args.cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_budget_s)
+    return out
+
+
+def bipartite_graph(scale=20, l=None, r=None):
+    """The C4 matching network (scale 20) or a bounded CPU sample of it: the same recipe at
+    2^scale x 2^scale with 2^(scale+4) draws."""
+    import synth
+    from oracle import matching
+    if l is None:
+        l, r = synth.bipartite_edges(1 << scale, 1 << scale, 1 << (scale + 4), 1)
+    n, src, dst, cap, s, t = matching.network(1 << scale, 1 << scale, l, r)
+    return synth.from_edges(n, src, dst, cap, s, t, name=f"c4-network-2^{scale}")
+
+
 def cpu_baseline(wl, budget_s):
     """The oracle as it stands (oracle/, single thread) on a bounded sample of the workload."""
     import oracle
+    if wl["kind"] == "bipartite":
+        g = bipartite_graph(20, wl["l"], wl["r"])
+        r = oracle.maxflow_graph(g, phase2=False)
+        return {"value": round(1.0 / r.seconds, 4), "unit": "matchings/s", "cores": 1, "kind": "oracle",
+                "sample": f"the C4 instance itself, one matching: {r.seconds:.2f} s of single-thread oracle "
+                          "solve time (ingest excluded)", "cpu": cpu_model(), "nproc": os.cpu_count()}
     parts = wl["parts"] if wl["kind"] == "batch" else [wl["graph"]]
     done, t_sum = 0, 0.0
     for g in parts:
@@ -345,7 +472,10 @@ def run_reference(args, rank, world):
         return None
     import oracle
     wl = make_workload(args.workload, 0, 1)
-    parts = wl["parts"] if wl["kind"] == "batch" else [wl["graph"]]
+    if wl["kind"] == "bipartite":
+        parts = [bipartite_graph(20, wl["l"], wl["r"])]   # the C4 network itself (~12 s per oracle solve)
+    else:
+        parts = wl["parts"] if wl["kind"] == "batch" else [wl["graph"]]
     i = 0
 
     def step():
@@ -360,7 +490,7 @@ def run_reference(args, rank, world):
     secs = [step() for _ in range(args.steps)]
     t = float(np.sum(secs))
     value = args.steps / t
-    unit = "instances/s" if wl["kind"] == "batch" else "solves/s"
+    unit = {"batch": "instances/s", "bipartite": "matchings/s"}.get(wl["kind"], "solves/s")
     return {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": unit, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3),
@@ -368,7 +498,8 @@ def run_reference(args, rank, world):
         "dtype": "int64", "data": "synthetic",
         "config": {"workload": args.workload, "desc": wl["desc"], "layout": "oracle arc-pair lists"},
         "cpu_baseline": {"value": round(value, 4), "unit": unit, "cores": 1, "kind": "oracle",
-                         "sample": f"{args.steps} instance solves of the workload (one per step, cycling)",
+                         "sample": f"{args.steps} instance solves of the workload (one per step, cycling)"
+                                   + (" - the full C4 network per step" if wl["kind"] == "bipartite" else ""),
                          "cpu": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": round(value, 4), "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -379,7 +510,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c5", choices=["c5", "c1", "c2", "c2r", "c3", "c3h"])
+    ap.add_argument("--workload", default="c5", choices=["c5", "c1", "c2", "c2r", "c3", "c3h", "c4"])
     ap.add_argument("--layout", default="bcsr", choices=["bcsr", "rcsr"])
     ap.add_argument("--impl", default="wbpr", choices=["wbpr", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
