@@ -264,31 +264,47 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_tile(K* keys, const int2*
 }
 
 // One merge pass of width w over every big segment (one CTA per segment).
+// One merge pass of width w over every big segment: one CTA per segment when there are
+// many, else every segment in turn by the whole grid (a 2^20-entry hub list would
+// otherwise be merged by a single CTA).  Each thread emits 8 outputs from its co-rank.
+template <typename K>
+__device__ __forceinline__ void merge_pass_task(const K* __restrict__ src, K* dst, int beg, int len, int w, int tk) {
+  int kk = tk << 3;
+  int pair0 = kk / (2 * w) * (2 * w);
+  int la = min(w, len - pair0);
+  int lb = min(w, len - pair0 - la);
+  if (lb < 0) lb = 0;
+  const K* A = src + beg + pair0;
+  const K* B = A + la;
+  int k = kk - pair0;
+  int i = co_rank<K>(k, A, la, B, lb);
+  int j = k - i;
+  int outn = min(8, la + lb - k);
+  K* O = dst + beg + kk;
+  for (int q = 0; q < outn; ++q) {
+    bool takeA = j >= lb || (i < la && A[i] <= B[j]);
+    O[q] = takeA ? A[i++] : B[j++];
+  }
+}
+
 template <typename K>
 __global__ void __launch_bounds__(256) k_merge_pass(const K* __restrict__ src, K* dst, const int* __restrict__ off,
                                                     const int* __restrict__ big, const int* count, int w) {
-  int nbig = *count;
-  for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
-    int sgi = big[bi];
-    int beg = off[sgi], len = off[sgi + 1] - beg;
-    int ntask = (len + 7) >> 3;
-    for (int tk = threadIdx.x; tk < ntask; tk += blockDim.x) {
-      int kk = tk << 3;
-      int pair0 = kk / (2 * w) * (2 * w);
-      int la = min(w, len - pair0);
-      int lb = min(w, len - pair0 - la);
-      if (lb < 0) lb = 0;
-      const K* A = src + beg + pair0;
-      const K* B = A + la;
-      int k = kk - pair0;
-      int i = co_rank<K>(k, A, la, B, lb);
-      int j = k - i;
-      int outn = min(8, la + lb - k);
-      K* O = dst + beg + kk;
-      for (int q = 0; q < outn; ++q) {
-        bool takeA = j >= lb || (i < la && A[i] <= B[j]);
-        O[q] = takeA ? A[i++] : B[j++];
-      }
+  const int nbig = *count;
+  if (nbig >= (int)gridDim.x / 4) {
+    for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+      int sgi = big[bi];
+      int beg = off[sgi], len = off[sgi + 1] - beg;
+      int ntask = (len + 7) >> 3;
+      for (int tk = threadIdx.x; tk < ntask; tk += blockDim.x) merge_pass_task<K>(src, dst, beg, len, w, tk);
+    }
+  } else {
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+    for (int bi = 0; bi < nbig; ++bi) {
+      int sgi = big[bi];
+      int beg = off[sgi], len = off[sgi + 1] - beg;
+      int ntask = (len + 7) >> 3;
+      for (int tk = gt; tk < ntask; tk += T) merge_pass_task<K>(src, dst, beg, len, w, tk);
     }
   }
 }
@@ -296,11 +312,12 @@ __global__ void __launch_bounds__(256) k_merge_pass(const K* __restrict__ src, K
 template <typename K>
 __global__ void __launch_bounds__(256) k_copy_big(const K* __restrict__ src, K* dst, const int* __restrict__ off,
                                                   const int* __restrict__ big, const int* count) {
-  int nbig = *count;
-  for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+  const int nbig = *count;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
+  for (int bi = 0; bi < nbig; ++bi) {
     int sgi = big[bi];
     int beg = off[sgi], len = off[sgi + 1] - beg;
-    for (int i = threadIdx.x; i < len; i += blockDim.x) dst[beg + i] = src[beg + i];
+    for (int i = gt; i < len; i += T) dst[beg + i] = src[beg + i];
   }
 }
 

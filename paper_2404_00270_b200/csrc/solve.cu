@@ -69,6 +69,12 @@ struct BcsrOps {
     atomicAdd(&arc[slot].y, -d);
     atomicAdd(&arc[__ldg(mate + slot)].y, d);
   }
+  // the reverse-arc lookup of a push, loadable ahead of the push (latency-bound phases)
+  __device__ int aux(int slot) const { return ld_nc_hint(mate + slot, pf); }
+  __device__ void push_aux(int slot, int ax, int d) const {
+    atomicAdd(&arc[slot].y, -d);
+    atomicAdd(&arc[ax].y, d);
+  }
   __device__ void saturate(int slot, int d) const { push(slot, d); }
 };
 
@@ -116,6 +122,11 @@ struct RcsrOps {
   __device__ void push(int slot, int d) const {
     if (slot < Mf) { atomicAdd(&farc[slot].y, -d); atomicAdd(bcf + slot, d); }
     else { int f = __ldg(&rarc[slot - Mf].y); atomicAdd(bcf + f, -d); atomicAdd(&farc[f].y, d); }
+  }
+  __device__ int aux(int slot) const { return slot < Mf ? slot : __ldg(&rarc[slot - Mf].y); }
+  __device__ void push_aux(int slot, int ax, int d) const {
+    if (slot < Mf) { atomicAdd(&farc[slot].y, -d); atomicAdd(bcf + slot, d); }
+    else { atomicAdd(bcf + ax, -d); atomicAdd(&farc[ax].y, d); }
   }
 };
 
@@ -321,17 +332,23 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       const unsigned target = gen + 1;
       int ab = 0;
       uint4 b;
-      unsigned old = atom_add_acqrel(&GC->bar.count, 1u);
-      if (old == nb - 1) {
+      // (a two-level arrival - 16 sub-counters - measured no faster on B200: the arrival
+      // atomics are not the bottleneck of a phase)
+      if (atom_add_acqrel(&GC->bar.count, 1u) == nb - 1) {
         GC->bar.count = 0;
         Ring* r = ring(ph);
-        const int qn = ld_cg(&r->qn), hc = ld_cg(&r->hc), kind = ld_cg(&r->kind);
+        // the whole phase record and the abort word in one round trip
+        const int4 r0 = ld_cg(reinterpret_cast<const int4*>(r));
+        const int4 r1 = ld_cg(reinterpret_cast<const int4*>(r) + 1);
+        const int abort_now = ld_volatile(&C->abort);
+        const int qn = r0.x, rhn = r0.y, hc = r0.z, kind = r1.x, rmaxdeg = r1.z;
+        const unsigned rwork = (unsigned)r0.w, rfedges = (unsigned)r1.y;
         const unsigned long long now = globaltimer();
         GrPolicy& G = GC->pol;
         unsigned flags = 0;
         if (kind == PK_ROUND) {
-          atomicAdd((unsigned long long*)&C->stats[ST_AVQ], (unsigned long long)(qn + ld_cg(&r->hn)));
-          G.work_since_gr += ld_cg(&r->work);
+          atomicAdd((unsigned long long*)&C->stats[ST_AVQ], (unsigned long long)(qn + rhn));
+          G.work_since_gr += rwork;
           // GR policy (reading §8(c) #8): queue empty, relabel work above
           // beta (n + M), or time spent in rounds since the last GR above gamma x its cost
           bool due = qn + hc == 0 || G.work_since_gr >= gr_threshold ||
@@ -347,7 +364,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           // direction-optimizing BFS (Beamer): bottom-up while the frontier's slots
           // exceed 1/14 of the slots not yet labelled; back to top-down when the
           // frontier holds fewer than n/24 vertices
-          const unsigned long long fe = ld_cg(&r->fedges);
+          const unsigned long long fe = rfedges;
           if (kind == PK_GR_RESET) { G.bfs_seen_edges = 0; G.bfs_bottom_up = 0; }
           G.bfs_seen_edges += fe;
           // slots still to be labelled: bounded by what the previous GR reached (vertices cut
@@ -374,7 +391,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           if (kind == PK_ROUND) next = (flags & 1) ? 0 : 1;
           else if (kind == PK_GR_RESET || kind == PK_BFS) next = (qn + hc > 0 && !(flags & 2)) ? 2 : 0;
           else if (kind == PK_COMPACT) next = (qn + hc > 0) ? 1 : 0;
-          const int md = ld_cg(&r->maxdeg);
+          const int md = rmaxdeg;
           if (P.small_mode && P.schedule == 0 && next && hc == 0 && qn > 0 && qn <= kSmallMax && md <= kSmallDeg) flags |= 4;
         }
         {   // phase timing: release of the previous barrier -> this release, by phase kind
@@ -386,12 +403,14 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           G.bfs_bottom_up_prev = (flags & 2) ? 1 : 0;
           G.t_release = now;
         }
+        if (abort_now) flags |= 16;
         b.x = target;
         b.y = (unsigned)qn;
         b.z = (unsigned)hc;
         b.w = flags;
         Ring* z = ring(ph + 1);
-        z->qn = 0; z->hn = 0; z->hc = 0; z->work = 0; z->kind = 0; z->fedges = 0; z->maxdeg = 0;
+        reinterpret_cast<int4*>(z)[0] = make_int4(0, 0, 0, 0);
+        reinterpret_cast<int4*>(z)[1] = make_int4(0, 0, 0, 0);
         st_release_v4(&GC->bc, b);
       } else {
         unsigned ns = 0;
@@ -404,7 +423,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           ns = ns ? (ns < 128 ? ns * 2 : 128) : 16;
         }
       }
-      if (!ab) ab = ld_volatile(&C->abort);
+      if (!ab) ab = (b.w & 16) != 0;   // the last arriver saw the abort word
       S.abort = ab;
       S.bc.qn = (int)b.y; S.bc.hc = (int)b.z; S.bc.flags = b.w;
     }
@@ -519,11 +538,16 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         cf[j] = 0; col[j] = 0; slot[j] = 0;
         if (b0 + j < d) ops.out_arc(sg, b0 + j, col[j], cf[j], slot[j]);
       }
-      int dgc[kSB];
+      // everything a push needs is loaded together with the labels (one round trip)
+      int dgc[kSB], axc[kSB];
+      uint8_t tmc[kSB];
 #pragma unroll
       for (int j = 0; j < kSB; ++j) {
+        const bool pre = P.push_mode != 0 && cf[j] > 0;
         hv[j] = cf[j] > 0 ? ld_h(P.h + col[j], pl) : INT_MAX;
-        dgc[j] = (P.push_mode != 0 && cf[j] > 0) ? ops.degree(col[j]) : 0;
+        dgc[j] = pre ? ops.degree(col[j]) : 0;
+        axc[j] = pre ? ops.aux(slot[j]) : 0;
+        tmc[j] = pre ? ld_term(P.term + col[j]) : 1;
       }
 #pragma unroll
       for (int j = 0; j < kSB; ++j) {
@@ -538,9 +562,9 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           if (cf[j] > 0 && hv[j] < hu && budget > 0) {
             int dd = (int)(budget < (long long)cf[j] ? budget : (long long)cf[j]);
             int dgv = dgc[j];
-            ops.push(slot[j], dd);
+            ops.push_aux(slot[j], axc[j], dd);
             long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col[j]), (unsigned long long)dd);
-            if (!tc && old_v == 0 && ld_term(P.term + col[j]) == 0) small_append(col[j], dgv);
+            if (!tc && old_v == 0 && tmc[j] == 0) small_append(col[j], dgv);
             budget -= dd;
             pushed += dd;
             ++st_push;
@@ -583,11 +607,17 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         cf[j] = 0; u[j] = 0;
         if (b0 + j < d) ops.in_arc(sg, b0 + j, u[j], cf[j]);
       }
+      // labels and degrees loaded with the residual capacities (one round trip; the graphs
+      // that reach the small mode are latency-bound)
+      int dgu[kSB];
 #pragma unroll
-      for (int j = 0; j < kSB; ++j) hu8[j] = cf[j] > 0 ? ld_h(P.h + u[j], pl) : -1;
+      for (int j = 0; j < kSB; ++j) {
+        hu8[j] = b0 + j < d ? ld_h(P.h + u[j], pl) : -1;
+        dgu[j] = b0 + j < d ? ops.degree(u[j]) : 0;
+      }
 #pragma unroll
       for (int j = 0; j < kSB; ++j)
-        if (cf[j] > 0 && hu8[j] == N && atomicCAS(P.h + u[j], N, lvl + 1) == N) small_append(u[j], ops.degree(u[j]));
+        if (cf[j] > 0 && hu8[j] == N && atomicCAS(P.h + u[j], N, lvl + 1) == N) small_append(u[j], dgu[j]);
     }
     st_bfs_arcs += d;
   };
@@ -626,11 +656,11 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         if (i < hi) ops.in_arc(sg, i, u[j], cf[j]);
       }
 #pragma unroll
-      for (int j = 0; j < kRU; ++j) hu[j] = cf[j] > 0 ? ld_h(P.h + u[j], pl) : -1;
+      for (int j = 0; j < kRU; ++j) hu[j] = (b + j * 32 + lane < hi) ? ld_h(P.h + u[j], pl) : -1;   // with c_f (parallel)
       bool found[kRU];
 #pragma unroll
       for (int j = 0; j < kRU; ++j)   // sinks 0, sources N+1: never N; level(u) = level(w) + 1
-        found[j] = hu[j] == N && atomicCAS(P.h + u[j], N, level + 1) == N;
+        found[j] = cf[j] > 0 && hu[j] == N && atomicCAS(P.h + u[j], N, level + 1) == N;
       int dg[kRU];
 #pragma unroll
       for (int j = 0; j < kRU; ++j) dg[j] = found[j] ? ops.degree(u[j]) : 0;
@@ -726,7 +756,8 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               }
               else if (spill) ex = 1;
             }
-            if (!ex && (ld_volatile(&C->abort) || now > deadline)) { atomicExch(&C->abort, 1); ex = 5; }
+            // (the abort word costs a dependent L2 round trip: polled every 64 phases)
+            if (!ex && (now > deadline || ((c_phases & 63) == 0 && ld_volatile(&C->abort)))) { atomicExch(&C->abort, 1); ex = 5; }
             S.s_exit = ex;
           }
           __syncthreads();
@@ -851,10 +882,10 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               }
               int hu[kBuB];
 #pragma unroll
-              for (int j = 0; j < kBuB; ++j) hu[j] = cf[j] > 0 ? ld_h(P.h + u[j], pl) : -1;
+              for (int j = 0; j < kBuB; ++j) hu[j] = (b0 + j < dthr) ? ld_h(P.h + u[j], pl) : -1;   // with c_f (parallel)
               bool found[kBuB];
 #pragma unroll
-              for (int j = 0; j < kBuB; ++j) found[j] = hu[j] == N && atomicCAS(P.h + u[j], N, level + 1) == N;
+              for (int j = 0; j < kBuB; ++j) found[j] = cf[j] > 0 && hu[j] == N && atomicCAS(P.h + u[j], N, level + 1) == N;
               int dg[kBuB];
 #pragma unroll
               for (int j = 0; j < kBuB; ++j) dg[j] = found[j] ? ops.degree(u[j]) : 0;
@@ -1139,6 +1170,13 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             }
 #pragma unroll
             for (int j = 0; j < kRU; ++j) hv[j] = cf[j] > 0 ? ld_h(P.h + col[j], pl) : INT_MAX;
+            // a task of <= 32 slots (road-like / matching graphs: latency-bound rounds) loads the
+            // reverse-arc lookup, terminal flag and degree of every residual arc together with
+            // the labels, so a push costs no further dependent round trips
+            const bool shortt = hi - lo <= 32;
+            int ax0 = 0, dg0 = 0;
+            uint8_t tm0 = 1;
+            if (shortt && cf[0] > 0) { ax0 = ops.aux(slot[0]); dg0 = ops.degree(col[0]); tm0 = ld_term(P.term + col[0]); }
             long long want = 0;            // admissible capacity of the whole super-group
             unsigned amask = 0;            // groups with an admissible arc
 #pragma unroll
@@ -1182,7 +1220,8 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               before += __shfl_sync(FULL, incl, 31);
               const long long d = adm ? (avail - excl < c ? avail - excl : c) : 0;
               if (d > 0) {
-                ops.push(slot[j], (int)d);
+                if (shortt && j == 0) ops.push_aux(slot[0], ax0, (int)d);
+                else ops.push(slot[j], (int)d);
                 oldv[j] = (long long)atomicAdd((unsigned long long*)(P.e + col[j]), (unsigned long long)d);
                 ++st_push;
               }
@@ -1193,10 +1232,11 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             // a push that raised e(v) from 0 appends v (exactly once, atomics on e)
             bool app[kRU];
 #pragma unroll
-            for (int j = 0; j < kRU; ++j) app[j] = oldv[j] == 0 && ld_term(P.term + col[j]) == 0;
+            for (int j = 0; j < kRU; ++j)
+              app[j] = oldv[j] == 0 && ((shortt && j == 0) ? tm0 == 0 : ld_term(P.term + col[j]) == 0);
             int dgv[kRU];
 #pragma unroll
-            for (int j = 0; j < kRU; ++j) dgv[j] = app[j] ? ops.degree(col[j]) : 0;
+            for (int j = 0; j < kRU; ++j) dgv[j] = app[j] ? ((shortt && j == 0) ? dg0 : ops.degree(col[j])) : 0;
 #pragma unroll
             for (int j = 0; j < kRU; ++j) {
               if (!((amask >> j) & 1u)) continue;
