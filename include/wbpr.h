@@ -7,7 +7,8 @@
  * the vertex-centric lock-free push-relabel loop of Alg. 1 and
  * Alg. 2 over the bidirectional / reversed CSR residual layouts of
  * §3.2, entirely on the device:
- *   A1 residual construction  (BCSR/RCSR + reverse-arc index by segmented sort)
+ *   A1 residual construction  (BCSR/RCSR; in-lists by segmented sort, reverse-arc index
+ *                              from the edge ids carried through the merge)
  *   A2 preflow                (Alg. 1 Step 0)
  *   A3 active-vertex queue    (Alg. 2 lines 1-5)
  *   A4 push/relabel           (Alg. 1 lines 9-21 with the relaxed rule P:187-189,
@@ -208,7 +209,7 @@ wbpr_status wbpr_bipartite_match(int64_t nL, int64_t nR, int64_t E, const int32_
 typedef struct wbpr_residual {
   int32_t layout;
   int64_t n, M, Mf;
-  const int32_t* off;   /* BCSR [n+1] / RCSR forward offsets [n+1] */
+  const int32_t* off;   /* RCSR forward offsets [n+1]; BCSR: NULL (see seg) */
   const int32_t* arc;   /* int2 pairs: BCSR [M] / RCSR forward [Mf] */
   const int32_t* mate;  /* BCSR [M] */
   const int32_t* cap0;  /* initial cf: BCSR [M] / RCSR forward [Mf] */

@@ -1,8 +1,10 @@
 // build.cu — K-BUILD (A1): device-side construction of the residual layouts of
 // PAPER.md §3.2 (Fig. 2):
 //   BCSR  one merged, column-sorted segment per vertex with its in- and out-arcs
-//          plus mate[p] = slot of the reverse arc: the paper's per-push
-//         binary search done once here (reading §8(c) #12).
+//         (gapped: segments in vertex order, unused slots between them,
+//         seg[u] = {begin, end}) plus mate[p] = slot of the reverse arc: the paper's
+//         per-push binary search replaced by edge identities carried
+//         through the construction (reading §8(c) #12; merge.cu, k_mate below).
 //   RCSR  forward CSR + reversed CSR whose entries carry flow_idx.
 // Readings: parallel edges summed, antiparallel pairs share one BCSR arc
 // pair, self-loops dropped and counted, zero-capacity pairs kept.

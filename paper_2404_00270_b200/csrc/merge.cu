@@ -5,15 +5,22 @@
 // residual capacity 0).  Instead of sorting the concatenation:
 //   * out-rows are taken in input order and sorted only where the input row is not
 //     already column-sorted (detected per row while the 64-bit keys are written);
-//   * in-lists carry 32-bit source ids only (their capacity is always 0), scattered
-//     by a histogram + atomic cursor and sorted with the 32-bit segmented sort;
-//   * a merge pass counts the distinct columns per vertex (parallel edges and
-//     antiparallel pairs collapse), a scan over n gives the final offsets,
-//     and a second merge pass writes {col, cf = sum of caps} and cap0.
+//   * in-lists carry the 32-bit INDEX e of the input edge (its capacity is always 0),
+//     scattered by a histogram + atomic cursor and sorted with the 32-bit segmented sort
+//     (sorting by e orders an in-list by source, rows being stored in vertex order);
+//     k_in_resolve then writes the source u = src[e] beside e;
+//   * one merge pass writes {col, cf = sum of caps} and cap0 (parallel edges and
+//     antiparallel pairs collapse) into a GAPPED layout: seg(x) starts at
+//     outdeg-prefix(x) + indeg-prefix(x), an upper bound of the distinct columns before
+//     x, so no counting pass or offset scan is needed; seg[x] = {begin, end};
+//   * the merge records the slot of every out-half-arc (outslot[e]) and of every in-list
+//     entry (inslot[t]); mate[] is then one lookup per input edge (build.cu k_mate) -
+//     the paper's backward-arc binary search is never run.
 // Merge classes: <= 32 elements: one thread, sequential two-pointer merge;
 // <= 8192: one warp, merge path advanced 32 outputs at a time with the 32-element
 // windows of both lists held in registers (co-rank by shuffles); larger: split into
-// 4096-output warp tasks whose starts come from a global co-rank search.
+// 4096-output warp tasks whose starts come from a global co-rank search (their counts
+// come from a counting pass over those hub vertices only).
 #include <climits>
 
 #include "internal.h"
