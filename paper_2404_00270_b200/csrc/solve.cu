@@ -921,9 +921,19 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         } else {
           // ---- bottom-up: every unlabelled vertex v looks for an out-arc v -> w with
           // c_f > 0 and level(w) = level (early exit per 32-slot group)
-          for (int base = VLO + gwarp * 32; base < VHI; base += nwarps * 32) {
+          // the label / frozen flag of the next 32-vertex group are loaded one iteration ahead
+          int nbase = VLO + gwarp * 32;
+          int hv_next = nbase + lane < VHI ? ld_cg_hint(P.h + nbase + lane, pl) : -1;
+          uint8_t fz_next = nbase + lane < VHI ? ld_term(P.deact + nbase + lane) : 1;
+          for (int base = nbase; base < VHI; base += nwarps * 32) {
             int v = base + lane;
-            int hv = v < VHI ? ld_cg_hint(P.h + v, pl) : -1;
+            const int hv = hv_next;
+            const uint8_t fz = fz_next;
+            {
+              const int nv = base + nwarps * 32 + lane;
+              hv_next = nv < VHI ? ld_cg_hint(P.h + nv, pl) : -1;
+              fz_next = nv < VHI ? ld_term(P.deact + nv) : 1;
+            }
             // low-degree vertices (<= kBuThread slots, the bulk of a power-law graph): one
             // THREAD per vertex, kBuB independent arc loads then kBuB label gathers per batch
             // (early exit per batch); larger ones below, one warp per vertex
@@ -931,7 +941,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             int dself = 0;
             Seg sv;
             sv.fb = sv.fe = sv.rb = sv.re = 0;
-            const bool unl = hv == N && !(phase == 1 && ld_term(P.deact + v));   // frozen: never reachable
+            const bool unl = hv == N && !(phase == 1 && fz);   // frozen: never reachable
             if (unl) { sv = ops.seg(v); dself = sv.deg(); }
             const bool thr = unl && dself <= kBuThread;
             if (thr) {
@@ -973,7 +983,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               }
             }
             bool found = (found_mask >> lane) & 1u;
-            int dg = found ? ops.degree(v) : 0;
+            int dg = found ? dself : 0;   // (dself = deg(v) for every unlabelled lane)
             unsigned fsum = warp_sum((unsigned)dg);
             if (lane == 0) fedges += fsum;
             warp_append(S, cnt, found, v, o, dg);
@@ -1020,6 +1030,13 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           for (int i = threadIdx.x; i < kGapBins; i += blockDim.x) S.gbin[i] = 0;
           __syncthreads();
         }
+        uint8_t c_tv = 1, c_fz = 1;
+        int c_hv = N;
+        long long c_ev = 0;
+        {
+          const int v0 = VLO + brank * blockDim.x + w * 32 + lane;
+          if (v0 < VHI) { c_tv = ld_term(P.term + v0); c_hv = ld_cg(P.h + v0); c_ev = ld_cg(P.e + v0); c_fz = ld_term(P.deact + v0); }
+        }
         for (int base = VLO + brank * blockDim.x + w * 32; base < VHI; base += nb * blockDim.x) {
           int v = base + lane;
           bool act = false, huge = false;
@@ -1029,16 +1046,23 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             if (hv0 < kGapBins) atomicAdd(&S.gbin[hv0], 1);
             else if (hv0 < N) atomicAdd(P.hist + hv0, 1);
           }
-          if (v < VHI && ld_term(P.term + v) == 0) {
-            const int hv = ld_cg(P.h + v);
-            const long long ev = ld_cg(P.e + v);
+          // terminal flag, label, excess and frozen flag: loaded one iteration ahead
+          const uint8_t tv = c_tv, fz = c_fz;
+          const int hv = c_hv;
+          const long long ev = c_ev;
+          {
+            const int nv = v + nb * blockDim.x;
+            c_tv = 1; c_fz = 1; c_hv = N; c_ev = 0;
+            if (nv < VHI) { c_tv = ld_term(P.term + nv); c_hv = ld_cg(P.h + nv); c_ev = ld_cg(P.e + nv); c_fz = ld_term(P.deact + nv); }
+          }
+          if (tv == 0) {
             if (hv < N) {
               if (ev > 0) {
                 act = true;
                 dg = ops.degree(v);
                 huge = dg > kChunk;
               }
-            } else if (phase == 1 && !ld_term(P.deact + v)) {
+            } else if (phase == 1 && !fz) {
               // v cannot reach a sink: it stays so for the rest of phase 1 (the set is closed,
               // §8(c) N5) - frozen: its excess leaves Excess_total once and later
               // bottom-up BFS levels skip it
@@ -1117,11 +1141,14 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       const int total = qn + hc;
       unsigned long long tt0; long long ta0, tp0, tr0c; int tn0;
       trace_begin(tt0, ta0, tp0, tr0c, tn0);
+      // the queue entry of a warp's next task is loaded while the current one runs
+      int u_next = gwarp < qn ? ld_cg(qc + gwarp) : 0;
       for (int tk = gwarp; tk < total; tk += nwarps) {
         ++tn0;
         int u, lo, hi, hidx = -1;
         if (tk < qn) {
-          u = ld_cg(qc + tk);
+          u = u_next;
+          if (tk + nwarps < qn) u_next = ld_cg(qc + tk + nwarps);
         } else {
           int2 c = ld_cg(hcc + (tk - qn));
           hidx = c.x;
