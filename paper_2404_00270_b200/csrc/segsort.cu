@@ -38,7 +38,48 @@ __global__ void __launch_bounds__(256) k_sort_warp(K* keys, const int* __restric
     int sgi = base + lane;
     int beg = 0, len = 0;
     if (sgi < nseg && (!need || need[sgi])) { beg = off[sgi]; len = off[sgi + 1] - beg; }
-    unsigned todo = __ballot_sync(FULL, len >= 2 && len <= 32);
+    // segments of <= 8 / <= 16 keys: 4 / 2 at a time, one 8- / 16-lane group each (rank
+    // sort over the group's lanes: 8 / 16 shuffles per key instead of 32)
+    unsigned t8 = __ballot_sync(FULL, len >= 2 && len <= 8);
+    while (t8) {
+      int jg[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) { jg[g] = t8 ? __ffs(t8) - 1 : -1; t8 &= t8 ? t8 - 1 : 0u; }
+      const int g = lane >> 3, sub = lane & 7;
+      const int j = g == 0 ? jg[0] : g == 1 ? jg[1] : g == 2 ? jg[2] : jg[3];
+      const int b = __shfl_sync(FULL, beg, j < 0 ? 0 : j), l0 = __shfl_sync(FULL, len, j < 0 ? 0 : j);
+      const int l = j < 0 ? 0 : l0;
+      K k = sub < l ? keys[b + sub] : key_max<K>();
+      int rank = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        K o = __shfl_sync(FULL, k, q, 8);
+        rank += (o < k) || (o == k && q < sub);
+      }
+      __syncwarp();
+      if (sub < l) keys[b + rank] = k;
+    }
+    unsigned t16 = __ballot_sync(FULL, len > 8 && len <= 16);
+    while (t16) {
+      const int j0 = __ffs(t16) - 1;
+      t16 &= t16 - 1;
+      const int j1 = t16 ? __ffs(t16) - 1 : -1;
+      if (t16) t16 &= t16 - 1;
+      const int sub = lane & 15;
+      const int j = lane < 16 ? j0 : j1;
+      const int b = __shfl_sync(FULL, beg, j < 0 ? 0 : j), l0 = __shfl_sync(FULL, len, j < 0 ? 0 : j);
+      const int l = j < 0 ? 0 : l0;
+      K k = sub < l ? keys[b + sub] : key_max<K>();
+      int rank = 0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        K o = __shfl_sync(FULL, k, q, 16);
+        rank += (o < k) || (o == k && q < sub);
+      }
+      __syncwarp();
+      if (sub < l) keys[b + rank] = k;
+    }
+    unsigned todo = __ballot_sync(FULL, len > 16 && len <= 32);
     while (todo) {
       int j = __ffs(todo) - 1;
       todo &= todo - 1;

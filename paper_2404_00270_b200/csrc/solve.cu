@@ -865,11 +865,16 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           // ones by the whole warp (td_warp_scan), hub chunks one warp per chunk task
           // (packing 32 entries per warp pays only when the frontier outnumbers the warps)
           const int per = qn >= nwarps * kTdPack ? 32 : 1;
+          // (the frontier entries of a warp's next iteration are loaded one iteration ahead)
+          const bool ldr = per == 32 || lane == 0;
+          int wv_next = (gwarp * per + (per == 32 ? lane : 0) < qn && ldr) ? ld_cg(qf + gwarp * per + (per == 32 ? lane : 0)) : 0;
           for (int base = gwarp * per; base < qn; base += nwarps * per) {
             const int tk = base + (per == 32 ? lane : 0);
             int wv = 0, dw = 0;
             Seg sw;
-            if (tk < qn && (per == 32 || lane == 0)) { wv = ld_cg(qf + tk); sw = ops.seg(wv); dw = sw.deg(); }
+            const int wv_cur = wv_next;
+            if (tk + nwarps * per < qn && ldr) wv_next = ld_cg(qf + tk + nwarps * per);
+            if (tk < qn && ldr) { wv = wv_cur; sw = ops.seg(wv); dw = sw.deg(); }
             const bool thr = per == 32 && tk < qn && dw <= kTdThread;
             const int dthr = thr ? dw : 0;
             if (thr) st_bfs_arcs += dw;   // per-thread partial (block-summed at the end)
