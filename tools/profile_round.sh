@@ -22,3 +22,8 @@ ncu --set full --clock-control none --import-source on -k regex:"k_merge_warp|k_
 python tools/ncu_summary.py $O/full_c5_build.ncu-rep > $O/full_c5_build_summary.txt 2>&1
 timeout 900 python tools/probe.py c1 c2u c2r c3p c3h c4 r18p r18h --reps 3 > $O/probe_bcsr.jsonl 2>&1
 python tools/phase_summary.py $O/probe_bcsr.jsonl > $O/probe_bcsr_phases.txt 2>&1
+timeout 1500 python tools/tc_vc_table.py --reps 3 > $O/tc_vc_table.md 2> $O/tc_vc_table.err
+timeout 900 python tools/workload_trace.py > $O/workload_trace.md 2> $O/workload_trace.err
+for G in 0.25 0.5 1 2; do
+  timeout 600 python tools/probe.py c5 c4 c3h --reps 2 --gamma $G > $O/gamma_$G.jsonl 2>&1
+done
