@@ -44,9 +44,10 @@ __global__ void __launch_bounds__(256) k_cutcap(const int64_t* __restrict__ ro, 
     const int u = warp_owner(ro, (int)n, ucur, ok ? i : E1 - 1);
     ucur = __shfl_sync(FULL, u, 31);
     if (!ok) continue;
+    if (ld_cg(h + u) < N) continue;        // u not in S*: the edge is not cut (skips col/cap)
     const int v = __ldg(col + i);
     const int c = __ldg(cap + i);
-    if (ld_cg(h + u) >= N && ld_cg(h + v) < N) {
+    if (ld_cg(h + v) < N) {
       if (u < ilo || u >= ihi) {
         if (acc) atomicAdd((unsigned long long*)(cut + inst), (unsigned long long)acc);
         acc = 0;

@@ -438,15 +438,26 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
   const long long* SNK = P.snk + I0;
   // ---------------------------------------------------------------- init
   if (brank == 0 && threadIdx.x == 0) GC->gap_level = N;
-  for (int v = VLO + brank * blockDim.x + threadIdx.x; v < VHI; v += nb * blockDim.x) {
-    st_cg(P.e + v, 0ll);
-    P.deact[v] = 0;
-    // static chunk list of the vertices with > kChunk slots (bottom-up BFS splits them)
-    int dg = ops.degree(v);
-    if (dg > kChunk) {
-      int nch = (dg + kChunk - 1) / kChunk;
-      int t0 = atomicAdd(&GC->nhs, nch);
-      for (int j = 0; j < nch; ++j) HS[t0 + j] = make_int2(v, j);
+  {   // 4 independent vertices per thread and iteration (memory-level parallelism)
+    const int stride = nb * blockDim.x;
+    for (int v0 = VLO + brank * blockDim.x + threadIdx.x; v0 < VHI; v0 += 4 * stride) {
+      int dgq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dgq[q] = v0 + q * stride < VHI ? ops.degree(v0 + q * stride) : 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int v = v0 + q * stride;
+        if (v >= VHI) continue;
+        st_cg(P.e + v, 0ll);
+        P.deact[v] = 0;
+        // static chunk list of the vertices with > kChunk slots (bottom-up BFS splits them)
+        const int dg = dgq[q];
+        if (dg > kChunk) {
+          int nch = (dg + kChunk - 1) / kChunk;
+          int t0 = atomicAdd(&GC->nhs, nch);
+          for (int j = 0; j < nch; ++j) HS[t0 + j] = make_int2(v, j);
+        }
+      }
     }
   }
   if (!gsync()) return;
@@ -823,9 +834,21 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
     if (state == S_GR) {
       // ------------------------------------------------------------ global relabel
       // reset labels: sinks 0, everything else |V| (= unreached); frontier <- sinks
-      for (int v = VLO + brank * blockDim.x + threadIdx.x; v < VHI; v += nb * blockDim.x) {
-        st_cg(P.h + v, (ld_term(P.term + v) & kSink) ? 0 : ((ld_term(P.term + v) & kSource) ? N + 1 : N));
-        if (P.gap_mode) st_cg(P.hist + v, 0);
+      {   // 4 independent vertices per thread and iteration (memory-level parallelism)
+        const int stride = nb * blockDim.x;
+        for (int v0 = VLO + brank * blockDim.x + threadIdx.x; v0 < VHI; v0 += 4 * stride) {
+          uint8_t tv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) tv[q] = v0 + q * stride < VHI ? ld_term(P.term + v0 + q * stride) : 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int v = v0 + q * stride;
+            if (v < VHI) {
+              st_cg(P.h + v, (tv[q] & kSink) ? 0 : ((tv[q] & kSource) ? N + 1 : N));
+              if (P.gap_mode) st_cg(P.hist + v, 0);
+            }
+          }
+        }
       }
       if (brank == 0) {
         QueueOut o = out_for(0);

@@ -317,3 +317,20 @@ def test_trace_vc_balances_better_than_tc():
                 vals.append((b / b.mean()).std())
         spread[sch] = float(np.median(vals))
     assert spread["vc"] < spread["tc"], spread
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_phase_timing_consistency(layout):
+    """wbpr_stats.phase_ns / phase_count: one GR reset and one compaction per global
+    relabel, every grid-wide round counted, times positive and within the solve window."""
+    g = synth.rmat(14, 16, 7, "hub20")
+    F, words, st, _ = gpu_solve(g, layout)
+    ref = oracle.maxflow_graph(g, phase2=False)
+    assert F == ref.flow
+    pc, pn = st["phase_count"], st["phase_ns"]
+    assert pc[2] == st["global_relabels"] == pc[4]
+    assert pc[5] == 1                                   # one preflow
+    assert pc[1] <= st["rounds"]                        # (small-mode rounds are counted in pc[8])
+    assert pc[3] + pc[7] <= st["bfs_levels"]
+    assert all(x >= 0 for x in pn) and sum(pn) > 0
+    assert sum(pn) <= st["solve_ms"] * 1e6 * 1.05
