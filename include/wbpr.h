@@ -95,7 +95,12 @@ typedef struct wbpr_options {
                             limit); 0 (default): off                                                */
   int32_t bfs_mode;      /* global-relabel BFS: 0 top-down only; 1 (default) direction-
                             optimizing (bottom-up levels while the frontier is large);
-                            2 bottom-up from the first level (testing)                      */
+                            2 bottom-up from the first level (testing); 3 direction-optimizing,
+                            and a GR deeper than 32 levels continues as an asynchronous
+                            label-correcting BFS (one shared work ring, no level barriers;
+                            converges to the same exact distances; measured ~2x slower than
+                            the level-synchronous BFS on grids - ring contention - so not
+                            the default)                                                     */
   int32_t small_mode;    /* 1 (default): phases whose queue fits one CTA (<= 512 vertices of
                             <= 8 slots) run in CTA 0 alone, one thread per vertex, with
                             block barriers instead of grid barriers; 0: off                 */
@@ -141,11 +146,12 @@ typedef struct wbpr_stats {
   int64_t kernel_launches;   /* kernels this call launched (all of them this library's own) */
   int64_t t_barrier_ns, t_flush_ns, t_round_ns; /* CTA 0 time in grid barriers / queue flushes /
                                                    round task loops (globaltimer)             */
-  int64_t phase_ns[9];       /* solve time by phase kind, barrier release to release
+  int64_t phase_ns[10];      /* solve time by phase kind, barrier release to release
                                 (globaltimer): 0 init, 1 push/relabel rounds, 2 GR label
                                 reset, 3 top-down BFS levels, 4 compactions, 5 preflow,
-                                6 gap lifts, 7 bottom-up BFS levels, 8 small-frontier spans */
-  int64_t phase_count[9];    /* phases per kind (small-frontier: phases run in CTA mode)  */
+                                6 gap lifts, 7 asynchronous GR continuation, 8 bottom-up
+                                BFS levels, 9 small-frontier spans                          */
+  int64_t phase_count[10];   /* phases per kind (small-frontier: phases run in CTA mode)  */
 } wbpr_stats;
 
 /* Fill *opt with the defaults above. */

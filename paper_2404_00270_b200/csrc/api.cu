@@ -311,6 +311,8 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.hq[0] = at<HugeRec>(ws, L.hq0); P.hq[1] = at<HugeRec>(ws, L.hq1);
   P.hc[0] = at<int2>(ws, L.hc0); P.hc[1] = at<int2>(ws, L.hc1);
   P.hist = at<int>(ws, L.hist);
+  P.aring = at<int2>(ws, L.aring);
+  P.inq = at<int>(ws, L.inq);
   P.hs = at<int2>(ws, L.hs);
   P.src = d_s; P.snk = d_t;
   P.max_rounds = opt.max_rounds > 0 ? opt.max_rounds : 10 * n + 1000;

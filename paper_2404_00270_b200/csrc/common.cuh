@@ -29,6 +29,21 @@ WBPR_DEV int4 ld_cg(const int4* p) { int4 v; asm volatile("ld.global.cg.v4.s32 {
 WBPR_DEV void st_cg(int* p, int v) { asm volatile("st.global.cg.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory"); }
 WBPR_DEV void st_cg(long long* p, long long v) { asm volatile("st.global.cg.s64 [%0], %1;" :: "l"(p), "l"(v) : "memory"); }
 
+WBPR_DEV int2 ld_acquire_v2(const int2* p) {
+  int2 v; asm volatile("ld.acquire.gpu.global.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory"); return v;
+}
+WBPR_DEV void st_release_v2(int2* p, int2 v) {
+  asm volatile("st.release.gpu.global.v2.s32 [%0], {%1,%2};" :: "l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+WBPR_DEV void st_cg_v2(int2* p, int2 v) {
+  asm volatile("st.global.cg.v2.s32 [%0], {%1,%2};" :: "l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+WBPR_DEV int atom_or_release(int* p, int v) {
+  int o; asm volatile("atom.release.gpu.global.or.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory"); return o;
+}
+WBPR_DEV int atom_exch_acquire(int* p, int v) {
+  int o; asm volatile("atom.acquire.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(o) : "l"(p), "r"(v) : "memory"); return o;
+}
 WBPR_DEV unsigned ld_acquire(const unsigned* p) {
   unsigned v; asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
 }

@@ -44,11 +44,12 @@ struct __align__(16) Bcast {
                     // bit 3: an online gap was found (lift phase before the next round)
 };
 
-enum PhaseKind { PK_NONE = 0, PK_ROUND = 1, PK_GR_RESET = 2, PK_BFS = 3, PK_COMPACT = 4, PK_PREFLOW = 5, PK_GAP = 6 };
+enum PhaseKind { PK_NONE = 0, PK_ROUND = 1, PK_GR_RESET = 2, PK_BFS = 3, PK_COMPACT = 4, PK_PREFLOW = 5, PK_GAP = 6,
+                 PK_ABFS = 7 };
 // phase-time buckets (Ctrl::phase_ns / phase_cnt): the PhaseKinds, plus
-constexpr int kPhBfsUp = 7;     // bottom-up BFS levels (PK_BFS counts the top-down ones)
-constexpr int kPhSmall = 8;     // small-frontier CTA-mode spans (CTA 0 alone)
-constexpr int kPhBuckets = 9;
+constexpr int kPhBfsUp = 8;     // bottom-up BFS levels (PK_BFS counts the top-down ones)
+constexpr int kPhSmall = 9;     // small-frontier CTA-mode spans (CTA 0 alone)
+constexpr int kPhBuckets = 10;
 
 // Global-relabel policy state, written only by the last CTA to arrive at a barrier.
 struct GrPolicy {
@@ -107,6 +108,11 @@ struct GroupCtrl {
   int gap_pending;         // the gap level the next lift phase uses
   int nhs;                 // entries of the static huge-chunk list
   int pad[3];
+  // asynchronous GR continuation (bfs_mode 3): ring head / tail / pending entries, each on
+  // its own 128-B line
+  int aq_head[32];
+  int aq_tail[32];
+  int aq_pending[32];
 };
 
 // Host-computed partition of the persistent grid into solver groups.
@@ -159,7 +165,7 @@ struct Layout {
   size_t ctrl, inst_s, inst_t, inst_flow, inst_cut, vbase;
   size_t in_row, in_col, in_cap;           // staging copy of a host CSR
   size_t h, e, term, deact, deg, cursor, off, soff, roff, rsoff, h1, seg;
-  size_t q0, q1, hq0, hq1, hc0, hc1, hist, hs;
+  size_t q0, q1, hq0, hq1, hc0, hc1, hist, hs, aring, inq;
   size_t scan_part;
   size_t regA, regB, regC;                 // build / residual regions
   size_t regD;                             // BCSR build: slot of every out-half-arc (4m B)
@@ -191,6 +197,7 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout, int32
   L.hq0 = take(sizeof(HugeRec) * hub); L.hq1 = take(sizeof(HugeRec) * hub);
   L.hc0 = take(8 * (2 * hub + 64)); L.hc1 = take(8 * (2 * hub + 64));
   L.hist = take(4 * (n + 2));
+  L.aring = take(8 * (n + 1)); L.inq = take(4 * (n + 1));   // asynchronous GR ring + in-queue flags
   L.hs = take(8 * (2 * hub + 64));
   L.scan_part = take(4 * ((H + 2 + n) / kScanTile + 64));
   L.regA = take(8 * H + 8);
@@ -234,6 +241,8 @@ struct SolveParams {
   HugeRec* hq[2];
   int2* hc[2];
   int* hist;
+  int2* aring;           // asynchronous GR: ring cells {seq, vertex} (slice [vlo, vhi) per group)
+  int* inq;              // asynchronous GR: 1 while the vertex is queued
   int2* hs;              // static (vertex, chunk) list of all vertices with > kChunk slots
   const long long* src; // sources [k]
   const long long* snk; // sinks [k]

@@ -354,8 +354,16 @@ template <typename K>
 __global__ void __launch_bounds__(256) k_copy_big(const K* __restrict__ src, K* dst, const int* __restrict__ off,
                                                   const int* __restrict__ big, const int* count) {
   const int nbig = *count;
+  if (nbig >= (int)gridDim.x / 4) {   // many big segments: one CTA each
+    for (int bi = blockIdx.x; bi < nbig; bi += gridDim.x) {
+      int sgi = big[bi];
+      int beg = off[sgi], len = off[sgi + 1] - beg;
+      for (int i = threadIdx.x; i < len; i += blockDim.x) dst[beg + i] = src[beg + i];
+    }
+    return;
+  }
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, T = gridDim.x * blockDim.x;
-  for (int bi = 0; bi < nbig; ++bi) {
+  for (int bi = 0; bi < nbig; ++bi) {   // few (hub) segments: the whole grid on each
     int sgi = big[bi];
     int beg = off[sgi], len = off[sgi + 1] - beg;
     for (int i = gt; i < len; i += T) dst[beg + i] = src[beg + i];

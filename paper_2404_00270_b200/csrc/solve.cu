@@ -162,7 +162,10 @@ constexpr int kGapBins = 256;     // online gap: shared-memory bins for the lowe
 #define WBPR_BUT 32
 #endif
 constexpr int kBuThread = WBPR_BUT; // bottom-up BFS: vertices up to this many slots are scanned by one thread
-constexpr int kBuB = 8;           // bottom-up BFS: slots loaded per batch (independent loads)
+#ifndef WBPR_BUB
+#define WBPR_BUB 8
+#endif
+constexpr int kBuB = WBPR_BUB;    // bottom-up BFS: slots loaded per batch (independent loads)
 // neighbour-label gathers: L2-only (default) or L1-allocating
 #ifndef WBPR_H_L1
 #define WBPR_H_L1 0   // measured: L1-allocating label gathers gave no gain (B200, C5/C3/C4)
@@ -170,6 +173,10 @@ constexpr int kBuB = 8;           // bottom-up BFS: slots loaded per batch (inde
 __device__ __forceinline__ int ld_h(const int* p, unsigned long long pol) {
   return WBPR_H_L1 ? ld_ca_hint(p, pol) : ld_cg_hint(p, pol);
 }
+constexpr int kAsyncLevel = 32;   // bfs_mode 3: a GR deeper than this continues asynchronously
+#ifndef WBPR_ASYNC_WARPS
+#define WBPR_ASYNC_WARPS 128         // warps taking part in the asynchronous GR continuation (best of 128/512/2048)
+#endif
 constexpr int kTdThread = 8;      // top-down BFS: frontier vertices up to this many slots are scanned by one thread
 constexpr int kTdPack = 4;        // top-down BFS: pack 32 frontier entries per warp when |frontier| >= kTdPack x warps
 #ifndef WBPR_RU
@@ -377,6 +384,8 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           else G.bfs_bottom_up = (long long)qn * 24 >= (long long)(VHI - VLO);
           if (P.bfs_mode == 2) G.bfs_bottom_up = 1;
           if (G.bfs_bottom_up) flags |= 2;
+          // bfs_mode 3: a deep GR continues as the asynchronous label-correcting BFS
+          if (P.bfs_mode == 3 && kind == PK_BFS && r1.w + 1 >= kAsyncLevel && qn + hc > 0) flags |= 32;
         } else if (kind == PK_COMPACT) {
           GC->gap_level = N;
           G.prev_reached = G.bfs_seen_edges;
@@ -687,7 +696,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
     }
   };
 
-  enum { S_GR = 0, S_BFS = 1, S_COMPACT = 2, S_ROUND = 3, S_DONE = 4 };
+  enum { S_GR = 0, S_BFS = 1, S_COMPACT = 2, S_ROUND = 3, S_DONE = 4, S_ABFS = 5 };
   int phase = 1;          // 2: return the stranded excess to the sources (NEXT #2)
   bool converged = false; // phase ended by an exact GR with no active vertex
   long long rounds = 0;
@@ -755,7 +764,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             if (state == S_BFS) {
               ++c_levels;
               if (nn == 0 && !S.s_huge) ex = 2;
-              else if (spill) ex = 1;
+              else if (spill || (P.bfs_mode == 3 && level + 1 >= kAsyncLevel)) ex = 1;
             } else {
               g_work += S.s_work;
               bool due = (nn == 0 && !S.s_huge) || g_work >= gr_threshold ||
@@ -869,6 +878,156 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       state = S_BFS;
       fb = 0;
       level = 0;
+      continue;
+    }
+
+    if (state == S_BFS && (S.bc.flags & 32)) { state = S_ABFS; continue; }
+
+    if (state == S_ABFS) {
+      // ------------------------------------------------------------ asynchronous GR continuation
+      // (bfs_mode 3, a GR deeper than kAsyncLevel levels).  The labels set so far are exact BFS
+      // distances and the frontier holds level `level`.  From here a label-correcting BFS runs
+      // over one bounded MPMC ring (cells {seq, v}: enqueue at position p waits for seq == p and
+      // writes p + 1, dequeue waits for p + 1 and frees the cell with p + cap) with no level
+      // barriers: a dequeued vertex w relaxes every residual in-arc u -> w,
+      // h(u) <- min(h(u), h(w) + 1), re-queueing u when it improves (in-queue flag: at most one
+      // ring entry per vertex, so cap = |group| cells suffice).  When nothing is pending, every
+      // label is its exact distance again (the Bellman-Ford fixed point over unit arcs), so the
+      // compaction, Excess_total and termination read the same labels as after the
+      // level-synchronous BFS.
+      const int fq = S.bc.qn, fh = S.bc.hc;     // the frontier (level `level`)
+      const int cap = VHI - VLO;
+      int2* const aring = P.aring + VLO;
+      for (int i = brank * blockDim.x + threadIdx.x; i < cap; i += nb * blockDim.x) {
+        st_cg_v2(aring + i, make_int2(i, 0));
+        st_cg(P.inq + VLO + i, 0);
+      }
+      if (brank == 0 && threadIdx.x == 0) {
+        GC->aq_head[0] = 0; GC->aq_tail[0] = 0; GC->aq_pending[0] = 0; ring(ph)->kind = PK_ABFS;
+      }
+      if (!gsync()) return;
+      // warp-collective enqueue of the lanes with pred (pending counted before the entries
+      // become visible, so pending == 0 means no entry queued and no vertex being processed)
+      auto aq_push = [&](bool pred, int v) {
+        const unsigned b = __ballot_sync(FULL, pred);
+        if (!b) return;
+        int base = 0;
+        if (lane == 0) {
+          atomicAdd(&GC->aq_pending[0], __popc(b));
+          base = atomicAdd(&GC->aq_tail[0], __popc(b));
+        }
+        base = __shfl_sync(FULL, base, 0);
+        __syncwarp();
+        if (pred) {
+          const int pos = base + __popc(b & lanemask_lt());
+          int2* const cell = aring + (pos % cap);
+          while (ld_acquire_v2(cell).x != pos) __nanosleep(20);
+          st_release_v2(cell, make_int2(pos + 1, v));
+        }
+      };
+      // seed: the frontier (normal entries and hub vertices, chunk 0 of each)
+      for (int t = gwarp * 32 + lane; t - lane < fq; t += nwarps * 32) {
+        const bool p = t < fq;
+        const int v = p ? ld_cg(Q[fb] + t) : 0;
+        if (p) st_cg(P.inq + v, 1);
+        aq_push(p, v);
+      }
+      for (int t = gwarp * 32 + lane; t - lane < fh; t += nwarps * 32) {
+        bool p = false;
+        int v = 0;
+        if (t < fh) {
+          const int2 c = ld_cg(HC[fb] + t);
+          if (c.y == 0) { p = true; v = ld_cg(&HQ[fb][c.x].u); st_cg(P.inq + v, 1); }
+        }
+        aq_push(p, v);
+      }
+      if (brank == 0 && threadIdx.x == 0) ring(ph)->kind = PK_ABFS;
+      if (!gsync()) return;
+      // the asynchronous loop: warps take up to 32 produced entries at a time (only the first
+      // kAsyncWarps warps take part: idle pollers would contend with the working ones)
+      unsigned idle_ns = 32;
+      while (gwarp < WBPR_ASYNC_WARPS) {
+        int base = 0, got = 0;
+        if (lane == 0) {
+          while (true) {
+            const int h0 = ld_volatile(&GC->aq_head[0]);
+            const int t0 = ld_volatile(&GC->aq_tail[0]);
+            if (h0 >= t0) break;
+            const int k = min(32, t0 - h0);
+            if (atomicCAS(&GC->aq_head[0], h0, h0 + k) == h0) { base = h0; got = k; break; }
+          }
+        }
+        base = __shfl_sync(FULL, base, 0);
+        got = __shfl_sync(FULL, got, 0);
+        if (got == 0) {
+          int stop = 0;
+          if (lane == 0) {
+            stop = ld_volatile(&GC->aq_pending[0]) == 0;
+            if (!stop && (globaltimer() > deadline || ld_volatile(&C->abort))) { atomicExch(&C->abort, 1); stop = 1; }
+          }
+          if (__shfl_sync(FULL, stop, 0)) break;
+          __nanosleep(idle_ns);
+          if (idle_ns < 1024) idle_ns <<= 1;
+          continue;
+        }
+        idle_ns = 32;
+        int w = -1;
+        if (lane < got) {
+          const int pos = base + lane;
+          int2* const cell = aring + (pos % cap);
+          int2 c = ld_acquire_v2(cell);
+          while (c.x != pos + 1) { __nanosleep(20); c = ld_acquire_v2(cell); }
+          w = c.y;
+          st_release_v2(cell, make_int2(pos + cap, 0));
+          atom_exch_acquire(P.inq + w, 0);   // dequeued: a later improvement of h(w) re-queues it
+        }
+        const int hw = w >= 0 ? ld_cg(P.h + w) : 0;
+        Seg sw;
+        sw.fb = sw.fe = sw.rb = sw.re = 0;
+        int dw = 0;
+        if (w >= 0) { sw = ops.seg(w); dw = sw.deg(); }
+        auto relax = [&](bool ok, int u, int cf, int hsrc) -> bool {   // true: u improved and must be queued
+          if (!ok || cf <= 0) return false;
+          const int nl = hsrc + 1;
+          if (ld_term(P.term + u) != 0 || ld_cg(P.h + u) <= nl) return false;
+          if (atomicMin(P.h + u, nl) <= nl) return false;
+          return atom_or_release(P.inq + u, 1) == 0;
+        };
+        // vertices with <= kTdThread slots: one thread each; larger ones: the whole warp
+        const bool thr = w >= 0 && dw <= kTdThread;
+        if (thr) st_bfs_arcs += dw;
+        for (int b0 = 0; __any_sync(FULL, thr && b0 < dw); b0 += kBuB) {
+          int u[kBuB], cf[kBuB];
+#pragma unroll
+          for (int j = 0; j < kBuB; ++j) {
+            u[j] = 0; cf[j] = 0;
+            if (thr && b0 + j < dw) ops.in_arc(sw, b0 + j, u[j], cf[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < kBuB; ++j) aq_push(relax(thr && b0 + j < dw, u[j], cf[j], hw), u[j]);
+        }
+        unsigned todo = __ballot_sync(FULL, w >= 0 && !thr);
+        while (todo) {
+          const int j = __ffs(todo) - 1;
+          todo &= todo - 1;
+          Seg sg;
+          sg.fb = __shfl_sync(FULL, sw.fb, j); sg.fe = __shfl_sync(FULL, sw.fe, j);
+          sg.rb = __shfl_sync(FULL, sw.rb, j); sg.re = __shfl_sync(FULL, sw.re, j);
+          const int hj = __shfl_sync(FULL, hw, j);
+          const int d = sg.deg();
+          if (lane == 0) st_bfs_arcs += d;
+          for (int b = 0; b < d; b += 32) {
+            int u = 0, cf = 0;
+            if (b + lane < d) ops.in_arc(sg, b + lane, u, cf);
+            aq_push(relax(b + lane < d, u, cf, hj), u);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) atomicAdd(&GC->aq_pending[0], -got);   // after this warp's pushes
+      }
+      if (brank == 0 && threadIdx.x == 0) { ++l_levels; ring(ph)->kind = PK_ABFS; }
+      if (!gsync()) return;
+      state = S_COMPACT;
       continue;
     }
 
@@ -1040,7 +1199,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           if (threadIdx.x == 0 && t) atomicAdd(&ring(ph)->fedges, (unsigned)t);
         }
         block_flush_all(S, cnt, o);
-        if (brank == 0 && threadIdx.x == 0) { ++l_levels; ring(ph)->kind = PK_BFS; }
+        if (brank == 0 && threadIdx.x == 0) { ++l_levels; ring(ph)->kind = PK_BFS; ring(ph)->pad = level; }
       }
       if (!gsync()) return;
       fb ^= 1;

@@ -56,7 +56,7 @@ class Stats(ctypes.Structure):
         ("build_ms", ctypes.c_float), ("solve_ms", ctypes.c_float), ("extract_ms", ctypes.c_float),
         ("total_ms", ctypes.c_float), ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int64), ("t_barrier_ns", ctypes.c_int64), ("t_flush_ns", ctypes.c_int64),
-        ("t_round_ns", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 9), ("phase_count", ctypes.c_int64 * 9)]
+        ("t_round_ns", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 10), ("phase_count", ctypes.c_int64 * 10)]
 
     def as_dict(self):
         d = {}

@@ -163,7 +163,7 @@ def test_gr_frequency_and_grid_size_invariance(layout):
 
 @pytest.mark.parametrize("layout", LAYOUTS)
 @pytest.mark.parametrize("push_mode", [0, 1])
-@pytest.mark.parametrize("bfs_mode", [0, 1, 2])
+@pytest.mark.parametrize("bfs_mode", [0, 1, 2, 3])
 @pytest.mark.parametrize("small_mode", [0, 1])
 @pytest.mark.parametrize("gap_mode", [0, 1])
 def test_modes(layout, push_mode, bfs_mode, small_mode, gap_mode):
@@ -330,7 +330,28 @@ def test_phase_timing_consistency(layout):
     pc, pn = st["phase_count"], st["phase_ns"]
     assert pc[2] == st["global_relabels"] == pc[4]
     assert pc[5] == 1                                   # one preflow
-    assert pc[1] <= st["rounds"]                        # (small-mode rounds are counted in pc[8])
-    assert pc[3] + pc[7] <= st["bfs_levels"]
+    assert pc[1] <= st["rounds"]                        # (small-mode rounds are counted in pc[9])
+    assert pc[3] + pc[8] <= st["bfs_levels"]
     assert all(x >= 0 for x in pn) and sum(pn) > 0
     assert sum(pn) <= st["solve_ms"] * 1e6 * 1.05
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("kind", ["grid", "rlg", "genrmf", "path"])
+def test_async_gr_deep_graphs(layout, kind):
+    """bfs_mode 3: GRs deeper than 32 levels continue as the asynchronous label-correcting
+    BFS; F, cut capacity and the canonical bitmap must stay bit-exact and the residual state
+    must pass V1-V7."""
+    if kind == "grid":
+        g = synth.grid(96, 64, True, 3)
+    elif kind == "rlg":
+        g = synth.washington_rlg(64, 32, 3, 1000, 2)
+    elif kind == "genrmf":
+        g = synth.genrmf(12, 10, 1, 1000, 4)
+    else:
+        k = 500
+        src = np.arange(k - 1); dst = src + 1
+        g = synth.from_edges(k, src, dst, np.full(k - 1, 3, np.int32), 0, k - 1)
+    F, st = assert_parity(g, layout, bfs_mode=3)
+    if kind != "path":
+        assert st["phase_count"][7] > 0, "the asynchronous continuation did not run"

@@ -1,7 +1,7 @@
 """Summarise tools/probe.py JSON lines: times, counters and the per-phase-kind breakdown.
 usage: python tools/phase_summary.py probe.jsonl"""
 import json, sys
-NAMES = ["init", "round", "gr_reset", "bfs_td", "compact", "preflow", "gap", "bfs_bu", "small"]
+NAMES = ["init", "round", "gr_reset", "bfs_td", "compact", "preflow", "gap", "bfs_async", "bfs_bu", "small"]
 for line in open(sys.argv[1]):
     try:
         d = json.loads(line)
