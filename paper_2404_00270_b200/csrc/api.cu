@@ -384,7 +384,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
       d.b0 = b0; d.nb = nbg[gi]; d.i0 = cut[gi]; d.i1 = cut[gi + 1];
       d.vlo = (int)vbase_h[d.i0]; d.vhi = (int)vbase_h[d.i1]; d.hub0 = (int)hub0;
       const int64_t mg = G == 1 ? m : eoff[d.i1] - eoff[d.i0];
-      hub0 += 2 * mg / kChunk + 64;
+      hub0 += 2 * mg / kMinChunk + 64;
       b0 += d.nb;
       groups.push_back(d);
     }

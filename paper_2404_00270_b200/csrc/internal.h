@@ -12,7 +12,12 @@ namespace wbpr {
 #ifndef WBPR_CHUNK
 #define WBPR_CHUNK 1024
 #endif
-constexpr int kChunk = WBPR_CHUNK; // slots per warp task; vertices with more slots are "huge"
+constexpr int kChunk = WBPR_CHUNK; // slots per warp task of a BFS level; vertices with more slots are "huge"
+#ifndef WBPR_RCHUNK
+#define WBPR_RCHUNK 512   // measured: 512 best on C5 (1024 / 256 slower or equal)
+#endif
+constexpr int kRChunk = WBPR_RCHUNK;   // slots per warp task of a push/relabel round
+constexpr int kMinChunk = kChunk < kRChunk ? kChunk : kRChunk;
 constexpr int kSortTile = 4096;    // CTA shared-memory sort tile (64-bit keys)
 constexpr int kScanTile = 4096;    // elements per scan tile
 constexpr int kMaxInst = 1 << 20;  // batch instances
@@ -193,7 +198,7 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout, int32
   L.off = take(4 * (n + 1)); L.soff = take(4 * (n + 1)); L.roff = take(4 * (n + 1)); L.rsoff = take(4 * (n + 1));
   L.seg = take(8 * n + 8);   // BCSR: {begin, end} of every vertex segment (gapped layout)
   L.q0 = take(4 * n + 4); L.q1 = take(4 * n + 4);
-  int64_t hub = H / kChunk + 64 * (k + 1);   // per-group slices (+64 slack each)
+  int64_t hub = H / kMinChunk + 64 * (k + 1);   // per-group slices (+64 slack each)
   L.hq0 = take(sizeof(HugeRec) * hub); L.hq1 = take(sizeof(HugeRec) * hub);
   L.hc0 = take(8 * (2 * hub + 64)); L.hc1 = take(8 * (2 * hub + 64));
   L.hist = take(4 * (n + 2));

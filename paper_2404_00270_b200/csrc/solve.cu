@@ -240,8 +240,8 @@ __device__ __forceinline__ void warp_append(SharedState& S, int& cnt, bool pred,
 }
 
 // a vertex with more than kChunk slots becomes nchunks warp tasks (single lane)
-__device__ __forceinline__ void huge_append(int u, int deg, const QueueOut& out) {
-  int nch = (deg + kChunk - 1) / kChunk;
+__device__ __forceinline__ void huge_append(int u, int deg, const QueueOut& out, int chunk) {
+  int nch = (deg + chunk - 1) / chunk;
   int hi = atomicAdd(out.hn, 1);
   int c0 = atomicAdd(out.hc_cnt, nch);
   HugeRec r; r.best = ~0ull; r.spent = 0; r.pushed = 0; r.u = u; r.nchunks = nch; r.done = 0; r.pad = 0;
@@ -526,12 +526,12 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
     }
   };
   int sa = 0, sdst = 0;   // shared-memory queue being read; global queue buffer being written
-  auto small_append = [&](int v, int dg) {
-    if (dg > kChunk) {
+  auto small_append = [&](int v, int dg, int chunk) {   // chunk: kChunk (BFS) / kRChunk (rounds)
+    if (dg > chunk) {
       QueueOut ho;
       ho.q = nullptr; ho.qn = nullptr; ho.md = nullptr;
       ho.hq = HQ[sdst]; ho.hc = HC[sdst]; ho.hn = &GC->small_hn; ho.hc_cnt = &GC->small_hc;
-      huge_append(v, dg, ho);
+      huge_append(v, dg, ho, chunk);
       S.s_huge = 1;
       return;
     }
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             int dgv = dgc[j];
             ops.push_aux(slot[j], axc[j], dd);
             long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col[j]), (unsigned long long)dd);
-            if (!tc && old_v == 0 && tmc[j] == 0) small_append(col[j], dgv);
+            if (!tc && old_v == 0 && tmc[j] == 0) small_append(col[j], dgv, kRChunk);
             budget -= dd;
             pushed += dd;
             ++st_push;
@@ -601,17 +601,17 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       ops.push((int)(best & 0xffffffffu), dd);
       long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-(long long)dd));
       long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + bcol), (unsigned long long)dd);
-      if (!tc && old_u - dd > 0) small_append(u, d);
-      if (!tc && old_v == 0 && ld_term(P.term + bcol) == 0) small_append(bcol, dgv);
+      if (!tc && old_u - dd > 0) small_append(u, d, kRChunk);
+      if (!tc && old_v == 0 && ld_term(P.term + bcol) == 0) small_append(bcol, dgv, kRChunk);
       ++st_push;
     } else if (P.push_mode != 0 && pushed > 0) {
       long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-pushed));
-      if (!tc && old_u - pushed > 0) small_append(u, d);
+      if (!tc && old_u - pushed > 0) small_append(u, d, kRChunk);
     } else {
       int nh = (best == ~0ull || (int)hmin >= N - 1) ? N : (int)hmin + 1;
       st_cg(P.h + u, nh);
       gap_relabel(hu, nh);
-      if (!tc && nh < N) small_append(u, d);
+      if (!tc && nh < N) small_append(u, d, kRChunk);
       if (tc) tc_work += (unsigned long long)d + 1;
       else atomicAdd(&S.s_work, (unsigned long long)d + 1);
       ++st_relabel;
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       }
 #pragma unroll
       for (int j = 0; j < kSB; ++j)
-        if (cf[j] > 0 && hu8[j] == N && atomicCAS(P.h + u[j], N, lvl + 1) == N) small_append(u[j], dgu[j]);
+        if (cf[j] > 0 && hu8[j] == N && atomicCAS(P.h + u[j], N, lvl + 1) == N) small_append(u[j], dgu[j], kChunk);
     }
     st_bfs_arcs += d;
   };
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         unsigned fsum = warp_sum((unsigned)dg[j]);
         if (lane == 0) fedges += fsum;
         const bool huge = found[j] && dg[j] > kChunk;
-        if (huge) huge_append(u[j], dg[j], o);
+        if (huge) huge_append(u[j], dg[j], o, kChunk);
         warp_append(S, cnt, found[j] && !huge, u[j], o, dg[j]);
       }
     }
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           int t = i < KI ? (int)SNK[i] : 0;
           int dg = i < KI ? ops.degree(t) : 0;
           bool huge = i < KI && dg > kChunk;
-          if (huge) huge_append(t, dg, o);
+          if (huge) huge_append(t, dg, o, kChunk);
           warp_append(S, cnt, i < KI && !huge, t, o, dg);
           unsigned fsum = warp_sum((unsigned)dg);
           if (lane == 0 && fsum) atomicAdd(&ring(ph)->fedges, fsum);
@@ -1082,7 +1082,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
                 unsigned fsum = warp_sum((unsigned)dg[j]);
                 if (lane == 0) fedges += fsum;
                 const bool huge = found[j] && dg[j] > kChunk;
-                if (huge) huge_append(u[j], dg[j], o);
+                if (huge) huge_append(u[j], dg[j], o, kChunk);
                 warp_append(S, cnt, found[j] && !huge, u[j], o, dg[j]);
               }
             }
@@ -1188,7 +1188,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             if (lane == 0) {
               st_bfs_arcs += scanned;
               if (hit && atomicCAS(P.h + vv, N, level + 1) == N) {
-                huge_append(vv, sg.deg(), o);
+                huge_append(vv, sg.deg(), o, kChunk);
                 fedges += sg.deg();
               }
             }
@@ -1247,7 +1247,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               if (ev > 0) {
                 act = true;
                 dg = ops.degree(v);
-                huge = dg > kChunk;
+                huge = dg > kRChunk;
               }
             } else if (phase == 1 && !fz) {
               // v cannot reach a sink: it stays so for the rest of phase 1 (the set is closed,
@@ -1258,7 +1258,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             }
           }
           if (lane == 0) st_cand += min(32, VHI - base);
-          if (huge) huge_append(v, dg, o);
+          if (huge) huge_append(v, dg, o, kRChunk);
           warp_append(S, cnt, act && !huge, v, o, dg);
         }
         block_flush_all(S, cnt, o);
@@ -1339,7 +1339,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         } else {
           int2 c = ld_cg(hcc + (tk - qn));
           hidx = c.x;
-          lo = c.y * kChunk;
+          lo = c.y * kRChunk;
           u = ld_cg(&hqc[hidx].u);
         }
         // independent loads issued together: segment bounds, h(u), e(u)
@@ -1347,7 +1347,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         const int hu = ld_cg(P.h + u);
         const long long eu = ld_cg(P.e + u);
         if (hu >= N) continue;   // lifted by the gap heuristic: inactive until the next GR
-        if (hidx < 0) { lo = 0; hi = sg.deg(); } else { hi = min(sg.deg(), lo + kChunk); }
+        if (hidx < 0) { lo = 0; hi = sg.deg(); } else { hi = min(sg.deg(), lo + kRChunk); }
         if (lane == 0) st_arcs += hi - lo;
 
         unsigned long long best = ~0ull;   // (h, slot) minimum over residual arcs (Alg. 1 l.10-13)
@@ -1454,8 +1454,8 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
 #pragma unroll
             for (int j = 0; j < kRU; ++j) {
               if (!((amask >> j) & 1u)) continue;
-              const bool hugev = app[j] && dgv[j] > kChunk;
-              if (hugev) huge_append(col[j], dgv[j], o);
+              const bool hugev = app[j] && dgv[j] > kRChunk;
+              if (hugev) huge_append(col[j], dgv[j], o, kRChunk);
               warp_append(S, cnt, app[j] && !hugev, col[j], o, dgv[j]);
             }
             if (hidx < 0 && budget <= 0) break;
@@ -1518,8 +1518,8 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             work += (unsigned long long)sg.deg() + 1;
             ++st_relabel;
           }
-          if (app_u >= 0 && dgu > kChunk) { huge_append(app_u, dgu, o); app_u = -1; }
-          if (app_v >= 0 && dgv > kChunk) { huge_append(app_v, dgv, o); app_v = -1; }
+          if (app_u >= 0 && dgu > kRChunk) { huge_append(app_u, dgu, o, kRChunk); app_u = -1; }
+          if (app_v >= 0 && dgv > kRChunk) { huge_append(app_v, dgv, o, kRChunk); app_v = -1; }
         }
         warp_append(S, cnt, lane == 0 && app_u >= 0, app_u, o, dgu);
         warp_append(S, cnt, lane == 0 && app_v >= 0, app_v, o, dgv);
