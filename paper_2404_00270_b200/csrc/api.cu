@@ -83,10 +83,47 @@ struct Ws {
   Ctrl* ctrl;
 };
 
+// Pinned staging for the small host <-> device copies of a call (terminals, instance ranges,
+// group descriptors, the control record, per-instance results).  Pageable copies are staged
+// by the driver and can serialise with other streams' transfers, which would stop one
+// caller thread's large H2D from overlapping another thread's kernels.  One buffer per host
+// thread, grown on demand; every call synchronises its stream before returning, so a region
+// is never reused while a copy from / to it is in flight.
+struct PinnedScratch {
+  char* p = nullptr;
+  size_t cap = 0;
+  ~PinnedScratch() { if (p) cudaFreeHost(p); }
+  char* get(size_t n) {
+    if (n > cap) {
+      if (p) cudaFreeHost(p);
+      cap = std::max<size_t>(n, size_t(1) << 16);
+      if (cudaHostAlloc(reinterpret_cast<void**>(&p), cap, cudaHostAllocPortable) != cudaSuccess) { p = nullptr; cap = 0; }
+    }
+    return p;
+  }
+};
+thread_local PinnedScratch g_pin;
+
+// device -> host through the pinned scratch at byte offset `at` (synchronous)
 wbpr_status read_ctrl(const Ctrl* d, Ctrl& h, cudaStream_t st) {
-  CK(cudaMemcpyAsync(&h, d, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  char* b = g_pin.get(sizeof(Ctrl));
+  if (!b) {
+    CK(cudaMemcpyAsync(&h, d, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return WBPR_OK;
+  }
+  CK(cudaMemcpyAsync(b, d, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  memcpy(&h, b, sizeof(Ctrl));
   return WBPR_OK;
+}
+
+// host -> device of a small array through pinned memory (offset `at` of the call's upload area)
+cudaError_t upload(void* dst, const void* src, size_t bytes, size_t at, cudaStream_t st) {
+  char* b = g_pin.get(at + bytes);
+  if (!b) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  memcpy(b + at, src, bytes);
+  return cudaMemcpyAsync(dst, b + at, bytes, cudaMemcpyHostToDevice, st);
 }
 
 wbpr_options resolve(const wbpr_options* o) {
@@ -263,9 +300,13 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   long long* d_s = at<long long>(ws, L.inst_s);
   long long* d_t = at<long long>(ws, L.inst_t);
   int64_t* d_vb = at<int64_t>(ws, L.vbase);
-  CK(cudaMemcpyAsync(d_s, s_h, 8 * k, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_t, t_h, 8 * k, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(d_vb, vbase_h, 8 * (k + 1), cudaMemcpyHostToDevice, st));
+  // (pinned upload area: [s | t | vbase | group descriptors]; read_ctrl's download uses the
+  //  start of the buffer only after the stream synchronised)
+  const size_t up_s = 0, up_t = 8 * (size_t)k, up_vb = 16 * (size_t)k, up_gd = 24 * (size_t)k + 8;
+  g_pin.get(up_gd + sizeof(GroupDesc) * (size_t)kMaxGroups + sizeof(Ctrl) + 16 * (size_t)k + 64);
+  CK(upload(d_s, s_h, 8 * k, up_s, st));
+  CK(upload(d_t, t_h, 8 * k, up_t, st));
+  CK(upload(d_vb, vbase_h, 8 * (k + 1), up_vb, st));
   uint8_t* term = at<uint8_t>(ws, L.term);
   CK(cudaMemsetAsync(term, 0, n, st));
   { k_terms<<<(k + 255) / 256, 256, 0, st>>>(term, d_s, d_t, k); note_launch(); }
@@ -389,8 +430,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
       groups.push_back(d);
     }
     blocks = b0;
-    CK(cudaMemcpyAsync(at<GroupDesc>(ws, L.gdesc), groups.data(), sizeof(GroupDesc) * groups.size(),
-                       cudaMemcpyHostToDevice, st));
+    CK(upload(at<GroupDesc>(ws, L.gdesc), groups.data(), sizeof(GroupDesc) * groups.size(), up_gd, st));
     CK(cudaMemsetAsync(at<GroupCtrl>(ws, L.gctrl), 0, sizeof(GroupCtrl) * groups.size(), st));
     P.groups = at<GroupDesc>(ws, L.gdesc);
     P.gctrl = at<GroupCtrl>(ws, L.gctrl);
@@ -449,14 +489,28 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   }
   CK(cudaGetLastError());
   std::vector<long long> hf(k), hc(k);
-  CK(cudaMemcpyAsync(hf.data(), d_flow, 8 * k, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hc.data(), d_cut, 8 * k, cudaMemcpyDeviceToHost, st));
+  // results through the pinned scratch (its upload area is free once the uploads completed,
+  // which the stream order guarantees before these copies run)
+  char* pin = g_pin.get(sizeof(Ctrl) + 16 * (size_t)k + 64);
+  Ctrl c;
+  if (pin) {
+    CK(cudaMemcpyAsync(pin + sizeof(Ctrl), d_flow, 8 * k, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pin + sizeof(Ctrl) + 8 * k, d_cut, 8 * k, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(hf.data(), d_flow, 8 * k, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hc.data(), d_cut, 8 * k, cudaMemcpyDeviceToHost, st));
+  }
   if (bitmap && g->on_host)
     CK(cudaMemcpyAsync(bitmap, dbm, 4 * ((n + 31) / 32), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(E.ev[3], st));
-  Ctrl c;
-  CK(cudaMemcpyAsync(&c, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  if (pin) CK(cudaMemcpyAsync(pin, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+  else CK(cudaMemcpyAsync(&c, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (pin) {
+    memcpy(&c, pin, sizeof(Ctrl));
+    memcpy(hf.data(), pin + sizeof(Ctrl), 8 * k);
+    memcpy(hc.data(), pin + sizeof(Ctrl) + 8 * k, 8 * k);
+  }
 
   const int M = opt.layout == WBPR_LAYOUT_BCSR ? c.M : 2 * Mf;
   register_view(W, opt.layout, M, opt.layout == WBPR_LAYOUT_BCSR ? c.M : Mf);
