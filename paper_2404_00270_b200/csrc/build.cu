@@ -112,11 +112,6 @@ __global__ void __launch_bounds__(256) k_edges(const int64_t* __restrict__ ro, c
   if (lane == 0 && loops) atomicAdd(&ctrl->selfloops, loops);
 }
 
-__global__ void k_add(int* a, const int* __restrict__ b, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    a[i] += b[i];
-}
-
 __global__ void k_maxlen(const int* __restrict__ deg, int64_t n, Ctrl* ctrl) {
   int mx = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -124,43 +119,6 @@ __global__ void k_maxlen(const int* __restrict__ deg, int64_t n, Ctrl* ctrl) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
   if (lane_id() == 0) atomicMax(&ctrl->maxlen, mx);
-}
-
-// BCSR scatter: out half-arc of edge i at soff[u] + (i - ro[u]) with key (v, c);
-// in half-arc at soff[v] + outdeg(v) + cursor[v]++ with key (u, 0).
-__global__ void k_scatter_bcsr(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
-                               const int32_t* __restrict__ cap, int64_t n, int64_t m,
-                               const int* __restrict__ soff, int* cursor, uint64_t* keys) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t i0 = t * kEdgesPerThread;
-  if (i0 >= m) return;
-  int64_t u = row_of(ro, n, i0);
-  int64_t i1 = i0 + kEdgesPerThread < m ? i0 + kEdgesPerThread : m;
-  for (int64_t i = i0; i < i1; ++i) {
-    while (__ldg(ro + u + 1) <= i) ++u;
-    int v = col[i], c = cap[i];
-    int64_t pos = soff[u] + (i - ro[u]);
-    if (v == u) { keys[pos] = kSent; continue; }
-    keys[pos] = ((uint64_t)(uint32_t)v << 32) | (uint32_t)c;
-    int vo = (int)(__ldg(ro + v + 1) - __ldg(ro + v));
-    int q = soff[v] + vo + atomicAdd(cursor + v, 1);
-    keys[q] = ((uint64_t)(uint32_t)u << 32);
-  }
-}
-
-// RCSR forward keys: the input CSR order is already the segment layout.
-__global__ void k_keys_fwd(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
-                           const int32_t* __restrict__ cap, int64_t n, int64_t m, uint64_t* keys) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t i0 = t * kEdgesPerThread;
-  if (i0 >= m) return;
-  int64_t u = row_of(ro, n, i0);
-  int64_t i1 = i0 + kEdgesPerThread < m ? i0 + kEdgesPerThread : m;
-  for (int64_t i = i0; i < i1; ++i) {
-    while (__ldg(ro + u + 1) <= i) ++u;
-    int v = col[i];
-    keys[i] = (v == u) ? kSent : (((uint64_t)(uint32_t)v << 32) | (uint32_t)cap[i]);
-  }
 }
 
 __global__ void k_ro_to_i32(const int64_t* __restrict__ ro, int64_t n, int* out) {
@@ -212,12 +170,6 @@ __global__ void k_merge_write(const uint64_t* __restrict__ keys, int64_t H, cons
     arc[slot] = make_int2((int)c, (int)sum);
     if (cap0) cap0[slot] = (int)sum;
   }
-}
-
-// Dense copy of the merged columns (region A, free after the merge) for the searches.
-__global__ void k_colcopy(const int2* __restrict__ arc, const Ctrl* ctrl, int* colv) {
-  const int M = ctrl->M;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < M; p += gridDim.x * blockDim.x) colv[p] = arc[p].x;
 }
 
 // mate[] from the edge identities carried through the construction (merge.cu): the
@@ -307,29 +259,6 @@ void build_validate(const BuildArgs& a, cudaStream_t st) {
                                                    a.layout == 0 ? a.tmp : a.keys, a.need,
                                                    a.layout == 0 ? a.src : nullptr); note_launch(); }
   { k_maxlen<<<grid_for(a.n, T, a.num_sms), T, 0, st>>>(a.deg, a.n, a.ctrl); note_launch(); }
-}
-
-// Phase 2 (after the host checked the validation record): sort, merge, mate.
-void build_bcsr(const BuildArgs& a, cudaStream_t st) {
-  const int T = 256;
-  const int64_t n = a.n, m = a.m;
-  // soff = exclusive scan of segment lengths
-  cudaMemcpyAsync(a.soff, a.deg, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
-  exclusive_scan(a.soff, n, a.scan_part, st);
-  const int64_t H = a.H;  // = soff[n], known on host
-  cudaMemsetAsync(a.cursor, 0, sizeof(int) * n, st);
-  int64_t threads = (m + kEdgesPerThread - 1) / kEdgesPerThread;
-  if (m > 0)
-    { k_scatter_bcsr<<<grid_exact(threads, T), T, 0, st>>>(a.ro, a.col, a.cap, n, m, a.soff, a.cursor, a.keys); note_launch(); }
-  segmented_sort(a.keys, a.tmp, a.soff, (int)n, a.maxlen, a.ctrl, a.arc, a.arc + a.H / 2, a.q0, a.num_sms, st);
-  int* flags = (int*)a.tmp;
-  cudaMemsetAsync(flags, 0, sizeof(int) * (H + 1), st);
-  { k_rowstarts<<<grid_for(n, T, a.num_sms), T, 0, st>>>(a.soff, n, flags); note_launch(); }
-  if (H > 0) { k_heads<<<grid_for(H, T, a.num_sms, 32), T, 0, st>>>(a.keys, H, flags); note_launch(); }
-  exclusive_scan(flags, H, a.scan_part, st);
-  { k_newoff<<<grid_for(n + 1, T, a.num_sms), T, 0, st>>>(a.soff, flags, n, a.off); note_launch(); }
-  if (H > 0) { k_merge_write<<<grid_for(H, T, a.num_sms, 32), T, 0, st>>>(a.keys, H, flags, a.arc, a.cap0, a.ctrl); note_launch(); }
-  cudaMemcpyAsync(&a.ctrl->M, flags + H, sizeof(int), cudaMemcpyDeviceToDevice, st);
 }
 
 void build_bcsr_mate(const BuildArgs& a, cudaStream_t st) {

@@ -61,10 +61,8 @@ struct BuildArgs {
 };
 
 void build_validate(const BuildArgs& a, cudaStream_t st);
-void build_bcsr(const BuildArgs& a, cudaStream_t st);
 void build_bcsr_mate(const BuildArgs& a, cudaStream_t st);
 void build_bcsr_merge(const BuildArgs& a, cudaStream_t st);
-void outkeys_need(const BuildArgs& a, uint64_t* keys, cudaStream_t st);
 void build_rcsr_forward(const BuildArgs& a, cudaStream_t st);
 void build_rcsr_reverse_counts(const BuildArgs& a, int Mf, cudaStream_t st);
 void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st);

@@ -43,27 +43,6 @@ __device__ __forceinline__ int row_of64(const int64_t* __restrict__ ro, int64_t 
   return (int)lo;
 }
 
-// 64-bit out-keys in input order; rows that are not non-decreasing get need[u] = 1.
-__global__ void k_outkeys(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
-                          const int32_t* __restrict__ cap, int64_t n, int64_t m, uint64_t* keys, uint8_t* need) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t i0 = t * 8;
-  if (i0 >= m) return;
-  int u = row_of64(ro, n, i0);
-  int64_t i1 = i0 + 8 < m ? i0 + 8 : m;
-  for (int64_t i = i0; i < i1; ++i) {
-    while (__ldg(ro + u + 1) <= i) ++u;
-    int v = col[i];
-    uint64_t k = (v == u) ? kSentKey : (((uint64_t)(uint32_t)v << 32) | (uint32_t)cap[i]);
-    keys[i] = k;
-    if (i > __ldg(ro + u)) {
-      int pv = col[i - 1];
-      uint64_t pk = (pv == u) ? kSentKey : (((uint64_t)(uint32_t)pv << 32) | (uint32_t)cap[i - 1]);
-      if (k < pk) need[u] = 1;
-    }
-  }
-}
-
 // in-list scatter: the out-half-arc at sorted row position e (edge u -> v, u != v)
 // lands in v's in-list as the 32-bit edge index e (sorting the in-list by e orders it by
 // the source u, since rows are stored in vertex order); k_in_resolve then turns e into
@@ -344,14 +323,6 @@ static unsigned gridcap(int64_t items, int threads, int num_sms, int per_sm) {
   int64_t b = (items + threads - 1) / threads;
   if (b > (int64_t)num_sms * per_sm) b = (int64_t)num_sms * per_sm;
   return (unsigned)(b < 1 ? 1 : b);
-}
-
-// 64-bit row keys in input order + per-row "needs sorting" flags (also used by RCSR).
-void outkeys_need(const BuildArgs& a, uint64_t* keys, cudaStream_t st) {
-  const int T = 256;
-  cudaMemsetAsync(a.need, 0, a.n, st);
-  int64_t threads = (a.m + 7) / 8;
-  if (a.m > 0) { k_outkeys<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(a.ro, a.col, a.cap, a.n, a.m, keys, a.need); note_launch(); }
 }
 
 // Build BCSR from the validated input (BuildArgs: deg = in-degrees, maxlen = max
