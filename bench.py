@@ -242,6 +242,7 @@ def run_wbpr(args, rank, world, local_rank):
     # bitmap inside every step).  Steps are issued by `args.e2e_streams` host threads, each with
     # its own stream and workspace (the public API used concurrently), so one step's H2D copy
     # overlaps another step's kernels; timed by wall clock between two device synchronizations.
+    # (--e2e-streams 0: no e2e leg - profiler runs whose last step must be a device-resident one)
     e2e_steps = max(1, min(args.steps, 5)) if args.e2e_streams <= 1 else max(2 * args.e2e_streams, min(args.steps, 8))
     pipes = []
     for _ in range(max(1, args.e2e_streams)):
@@ -256,13 +257,17 @@ def run_wbpr(args, rank, world, local_rank):
                 W.maxflow_batch(ro_h, col_h, cap_h, vbase, s, t, workspace=pp["ws"], bitmap=pp["bm"], device=dev,
                                 **opt)
 
+    if args.e2e_streams <= 0:
+        pipes = pipes[:0]
     for pp in pipes:            # warm each pipe once (workspace / stream first use)
         host_steps(pp, 1)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    if len(pipes) == 1:
+    if not pipes:
+        pass
+    elif len(pipes) == 1:
         host_steps(pipes[0], e2e_steps)
     else:
         per = [e2e_steps // len(pipes) + (1 if i < e2e_steps % len(pipes) else 0) for i in range(len(pipes))]
@@ -280,7 +285,7 @@ def run_wbpr(args, rank, world, local_rank):
     ms, e2e_ms = float(times[0]), float(times[1])
     total_units = wl["total"] if wl["kind"] == "batch" else world
     value = total_units * args.steps / (ms / 1e3)
-    e2e_value = total_units * e2e_steps / (e2e_ms / 1e3)
+    e2e_value = total_units * e2e_steps / (e2e_ms / 1e3) if args.e2e_streams > 0 else None
     if rank != 0:
         return None
     # certificate of every gathered record: F == cut capacity
@@ -337,7 +342,7 @@ def run_wbpr(args, rank, world, local_rank):
                      "build": {"kernels": "A1 construction (st['kernel_launches'] - 4 launches)",
                                "achieved": round(build_achieved, 2), "frac": round(build_achieved / hbm, 4),
                                "algorithmic_bytes": int(bb), "ms": round(build_ms, 3)}},
-        "e2e": {"value": round(e2e_value, 3), "unit": "instances/s" if wl["kind"] == "batch" else "solves/s",
+        "e2e": None if e2e_value is None else {"value": round(e2e_value, 3), "unit": "instances/s" if wl["kind"] == "batch" else "solves/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "pipelined_streams": max(1, args.e2e_streams), "timing": "wall clock between device syncs"},
         "gpu_launches": int(st["kernel_launches"]) * args.steps,

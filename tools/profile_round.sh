@@ -12,10 +12,10 @@ for W in c4 c3 c3h; do
   timeout 900 python bench.py --workload $W --steps 5 > $O/bench_$W.json 2> $O/bench_$W.err
 done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c5.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-streams 0 > /dev/null 2>&1
 python tools/launches.py $O/launches_c5.csv > $O/launches_c5_summary.txt 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_solve -s 3 -c 1 -o $O/full_c5_k_solve \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-streams 0 > /dev/null 2>&1
 python tools/ncu_summary.py $O/full_c5_k_solve.ncu-rep > $O/full_c5_k_solve_summary.txt 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_merge_warp|k_inscatter|k_mate|k_edges|k_merge_thread" \
     -c 6 -o $O/full_c5_build python tools/probe.py c5 --reps 1 > /dev/null 2>&1
