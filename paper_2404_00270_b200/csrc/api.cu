@@ -77,6 +77,8 @@ __global__ void k_terms(uint8_t* term, const long long* s, const long long* t, i
 
 template <typename T> T* at(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws) + off); }
 
+constexpr int64_t kSlotsPerCta = 32768;   // auto grid size for small graphs
+
 struct Ws {
   Layout L;
   void* base;
@@ -373,6 +375,14 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   if (occ < 1) return fail(WBPR_ECUDA, "solve kernel cannot be resident on this device");
   int blocks = di.num_sms * occ;
   if (opt.grid_blocks > 0 && opt.grid_blocks < blocks) blocks = opt.grid_blocks;
+  else if (opt.grid_blocks == 0) {
+    // auto: tiny graphs are phase-latency bound and a grid barrier over 296 CTAs costs more
+    // than the work of a phase: one CTA up to kSlotsPerCta residual slots (C1), one CTA per
+    // 2048 slots below the full grid (measured on C1, R-MAT-14, 128^2 grids, profiles/r1)
+    const int64_t slots = n + 2 * m;
+    const int64_t want = slots <= kSlotsPerCta ? 1 : slots / 2048 + 1;
+    if (want < blocks) blocks = (int)want;
+  }
 
   // ---- solver groups (A10): independent instances get disjoint CTA groups of the
   // persistent grid, sized by their edge counts, each with its own barrier and state

@@ -154,9 +154,18 @@ WBPR_DEV void st_release_v4(Bcast* p, uint4 v) {
 }
 
 constexpr int kSmallCap = 2048;   // small-frontier mode: shared-memory queue capacity
-constexpr int kSmallMax = 512;    // small-frontier mode: queues up to this size (one pass of 512 threads)
-constexpr int kSmallDeg = 8;      // small-frontier mode: largest degree processed by one thread
-constexpr int kSB = 4;            // small-frontier mode: slots loaded per batch (independent loads)
+#ifndef WBPR_SMALL_MAX
+#define WBPR_SMALL_MAX 512
+#endif
+constexpr int kSmallMax = WBPR_SMALL_MAX;   // small-frontier mode: queues up to this size (one pass of 512 threads)
+#ifndef WBPR_SMALL_DEG
+#define WBPR_SMALL_DEG 8
+#endif
+constexpr int kSmallDeg = WBPR_SMALL_DEG;   // small-frontier mode: largest degree processed by one thread
+#ifndef WBPR_SB
+#define WBPR_SB 4
+#endif
+constexpr int kSB = WBPR_SB;      // small-frontier mode: slots loaded per batch (independent loads)
 constexpr int kGapBins = 256;     // online gap: shared-memory bins for the lowest levels
 #ifndef WBPR_BUT
 #define WBPR_BUT 32

@@ -13,6 +13,10 @@ def graph(name):
     if name == "c2u": return synth.grid(1024, 1024, False, 1)
     if name == "c2r": return synth.grid(1024, 1024, True, 1)
     if name == "g256r": return synth.grid(256, 256, True, 1)
+    if name == "g128r": return synth.grid(128, 128, True, 1)
+    if name == "r14p": return synth.rmat(14, 16, 1, "paper")
+    if name == "r14h": return synth.rmat(14, 16, 1, "hub20")
+    if name == "rand16k": return synth.random_graph(16384, 131072, 1, 0, 16383)
     if name == "c3p": return synth.rmat(22, 16, 1, "paper")
     if name == "c3h": return synth.rmat(22, 16, 1, "hub20")
     if name == "r18p": return synth.rmat(18, 16, 1000, "paper")
