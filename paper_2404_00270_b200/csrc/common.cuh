@@ -63,6 +63,9 @@ WBPR_DEV unsigned long long policy_evict_last() {
 WBPR_DEV int2 ld_cg_hint(const int2* p, unsigned long long pol) {
   int2 v; asm volatile("ld.global.cg.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol)); return v;
 }
+WBPR_DEV int4 ld_cg_hint(const int4* p, unsigned long long pol) {
+  int4 v; asm volatile("ld.global.cg.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol)); return v;
+}
 WBPR_DEV int ld_cg_hint(const int* p, unsigned long long pol) {
   int v; asm volatile("ld.global.cg.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
 }
@@ -76,6 +79,9 @@ WBPR_DEV int ld_ca_hint(const int* p, unsigned long long pol) {
 }
 WBPR_DEV int ld_nc_hint(const int* p, unsigned long long pol) {
   int v; asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol)); return v;
+}
+WBPR_DEV int4 ld_nc_hint(const int4* p, unsigned long long pol) {
+  int4 v; asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol)); return v;
 }
 WBPR_DEV int2 ld_nc_hint(const int2* p, unsigned long long pol) {
   int2 v; asm volatile("ld.global.nc.L2::cache_hint.v2.s32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol)); return v;

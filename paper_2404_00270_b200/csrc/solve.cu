@@ -65,6 +65,30 @@ struct BcsrOps {
   __device__ void col_cf_of_slot(int slot, int& col, int& cf) const {
     int2 a = ld_cg(arc + slot); col = a.x; cf = a.y;
   }
+  // out-arcs b0 .. b0+7 of a segment with five 16-B loads (two arcs each, aligned down) instead
+  // of eight 8-B ones: one thread scanning its own segment issues fewer L1 wavefronts
+  static constexpr bool kVec8 = true;
+  }
+  __device__ void arcs8(const Seg& s, int b0, int d, int (&col)[8], int (&cf)[8]) const {
+    const int first = s.fb + b0;
+    const int a = first & ~1;
+    const bool odd = (first & 1) != 0;
+    int4 w[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const int p = a + 2 * q;
+      w[q] = p < s.fe ? ld_cg_hint(reinterpret_cast<const int4*>(arc + p), pf) : make_int4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      // arc j + odd of the window: even -> (x, y) of w[(j+odd)/2], odd -> (z, w)
+      const int4 e0 = w[j >> 1], e1 = w[(j + 1) >> 1];
+      const int c0 = (j & 1) ? e0.z : e0.x, f0 = (j & 1) ? e0.w : e0.y;      // arc j       (odd == 0)
+      const int c1 = (j & 1) ? e1.x : e0.z, f1 = (j & 1) ? e1.y : e0.w;      // arc j + 1   (odd == 1)
+      col[j] = odd ? c1 : c0;
+      cf[j] = b0 + j < d ? (odd ? f1 : f0) : 0;
+    }
+  }
   __device__ void push(int slot, int d) const {
     atomicAdd(&arc[slot].y, -d);
     atomicAdd(&arc[__ldg(mate + slot)].y, d);
@@ -79,6 +103,8 @@ struct BcsrOps {
 };
 
 struct RcsrOps {
+  static constexpr bool kVec8 = false;
+  __device__ void arcs8(const Seg&, int, int, int (&)[8], int (&)[8]) const {}
   const int* foff; int2* farc; const int* roff; const int2* rarc; int* bcf; int Mf;
   unsigned long long pf = 0;
   __device__ void init() { pf = policy_evict_first(); }
@@ -1071,6 +1097,8 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             if (thr) st_bfs_arcs += dw;   // per-thread partial (block-summed at the end)
             for (int b0 = 0; __any_sync(FULL, b0 < dthr); b0 += kBuB) {
               int u[kBuB], cf[kBuB];
+              // (16-B vector loads of the in-arcs, as the bottom-up scan does for out-arcs, were
+              //  measured slower here: the c_f gathers dominate and the selects cost issue slots)
 #pragma unroll
               for (int j = 0; j < kBuB; ++j) {
                 u[j] = 0; cf[j] = 0;
@@ -1144,10 +1172,14 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               int scanned = 0;
               for (int b0 = 0; b0 < dself && !self_hit; b0 += kBuB) {
                 int col[kBuB], cf[kBuB];
+                if constexpr (Ops::kVec8 && kBuB == 8) {
+                  ops.arcs8(sv, b0, dself, col, cf);
+                } else {
 #pragma unroll
-                for (int j = 0; j < kBuB; ++j) {
-                  col[j] = 0; cf[j] = 0;
-                  if (b0 + j < dself) { int slot; ops.out_arc(sv, b0 + j, col[j], cf[j], slot); }
+                  for (int j = 0; j < kBuB; ++j) {
+                    col[j] = 0; cf[j] = 0;
+                    if (b0 + j < dself) { int slot; ops.out_arc(sv, b0 + j, col[j], cf[j], slot); }
+                  }
                 }
                 int hl[kBuB];
 #pragma unroll
