@@ -68,7 +68,6 @@ struct BcsrOps {
   // out-arcs b0 .. b0+7 of a segment with five 16-B loads (two arcs each, aligned down) instead
   // of eight 8-B ones: one thread scanning its own segment issues fewer L1 wavefronts
   static constexpr bool kVec8 = true;
-  }
   __device__ void arcs8(const Seg& s, int b0, int d, int (&col)[8], int (&cf)[8]) const {
     const int first = s.fb + b0;
     const int a = first & ~1;
