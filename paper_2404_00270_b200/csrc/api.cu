@@ -182,6 +182,7 @@ wbpr_status build_residual(const Ws& W, const int64_t* ro, const int32_t* col, c
                                  " has a column outside its instance's range or a negative capacity");
   a.maxlen = c.maxlen;
   a.maxlen_out = c.maxlen_out;
+  a.any_unsorted = c.any_unsorted;
   if (layout == WBPR_LAYOUT_BCSR) {
     a.H = 2 * L.m - c.selfloops;
     build_bcsr_merge(a, st);

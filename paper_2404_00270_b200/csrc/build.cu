@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) k_edges(const int64_t* __restrict__ ro, c
     if (!ok) continue;
     keys[i] = key;
     if (src) src[i] = u;
-    if (pu == u && key < pk) need[u] = 1;
+    if (pu == u && key < pk) { need[u] = 1; ctrl->any_unsorted = 1; }
     if (k > 1 && (u < ilo || u >= ihi)) {
       int a = 0, b = k;
       while (b - a > 1) { int mid = (a + b) >> 1; if (__ldg(vbase + mid) <= u) a = mid; else b = mid; }

@@ -149,7 +149,7 @@ struct Ctrl {
   int sort_items_med;     // build scratch counter
   int mlist_w, mlist_c;   // build: vertices merged by a warp / by a CTA
   int maxlen_out;         // build: longest input row
-  int pad0[1];
+  int any_unsorted;       // build: some input row is not column-sorted (else the row sort is skipped)
   long long phase_ns[kPhBuckets];    // solve: barrier-release-to-release time per phase kind
   long long phase_cnt[kPhBuckets];
 };

@@ -52,6 +52,7 @@ struct BuildArgs {
   int* inslot;           // BCSR build: merged slot of every in-list entry (region A + 8m; src is dead by then)
   int* outslot;          // BCSR build: per out-half-arc (sorted row position), its merged slot (region D)
   int2* seg;             // BCSR: {begin, end} of every vertex segment
+  int any_unsorted;      // BCSR: some input row needs sorting (host copy of the validation flag)
   int* rsoff;            // BCSR merge build: in-list offsets
   uint8_t* need;         // BCSR merge build: per-row "not sorted" flags
   int* q1;

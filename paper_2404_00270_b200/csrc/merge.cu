@@ -343,8 +343,9 @@ void build_bcsr_merge(const BuildArgs& a, cudaStream_t st) {
   // out-keys, their sortedness flags and the edge owners (src) were written by the
   // validation pass (k_edges); rows not column-sorted are sorted first, so that the in-list
   // entries can name out-half-arcs by their sorted position
-  segmented_sort_filtered(outk, otmp, a.soff, (int)n, a.maxlen_out, a.need, a.ctrl, items, items_med, a.q0,
-                          a.num_sms, st);
+  if (a.any_unsorted)   // (validation found every row column-sorted: nothing to sort)
+    segmented_sort_filtered(outk, otmp, a.soff, (int)n, a.maxlen_out, a.need, a.ctrl, items, items_med, a.q0,
+                            a.num_sms, st);
   cudaMemcpyAsync(a.cursor, a.rsoff, sizeof(int) * n, cudaMemcpyDeviceToDevice, st);
   if (m > 0) {
     const int64_t sthreads = (m + kScatChunk - 1) / kScatChunk * 32;
