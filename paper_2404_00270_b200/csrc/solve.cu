@@ -216,7 +216,9 @@ constexpr int kTdPack = 4;        // top-down BFS: pack 32 frontier entries per 
 #ifndef WBPR_RU
 #define WBPR_RU 4
 #endif
-constexpr int kRU = WBPR_RU;      // push/relabel discharge: 32-slot groups loaded per iteration
+constexpr int kRU = WBPR_RU;
+constexpr int kRThr = 64;         // rounds: vertices up to this many slots are discharged by one thread ...
+constexpr int kRThrPack = 4;      // ... when the queue holds at least kRThrPack x warps entries      // push/relabel discharge: 32-slot groups loaded per iteration
 
 struct SharedState {
   int buf[kWarps][kBufCap];
@@ -447,6 +449,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           G.t_release = now;
         }
         if (abort_now) flags |= 16;
+        if (rmaxdeg <= kRThr) flags |= 64;   // every queued vertex is small: rounds may use the thread mode
         b.x = target;
         b.y = (unsigned)qn;
         b.z = (unsigned)hc;
@@ -1368,25 +1371,93 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       const int total = qn + hc;
       unsigned long long tt0; long long ta0, tp0, tr0c; int tn0;
       trace_begin(tt0, ta0, tp0, tr0c, tn0);
-      // the queue entry of a warp's next task is loaded while the current one runs
-      int u_next = gwarp < qn ? ld_cg(qc + gwarp) : 0;
-      for (int tk = gwarp; tk < total; tk += nwarps) {
-        ++tn0;
-        int u, lo, hi, hidx = -1;
-        if (tk < qn) {
-          u = u_next;
-          if (tk + nwarps < qn) u_next = ld_cg(qc + tk + nwarps);
-        } else {
-          int2 c = ld_cg(hcc + (tk - qn));
-          hidx = c.x;
-          lo = c.y * kRChunk;
-          u = ld_cg(&hqc[hidx].u);
+      // thread-serial discharge of vertex u (<= kRThr slots) by one lane: the same semantics as
+      // the warp discharge below (pushes to every admissible arc in slot order, budget split,
+      // relabel to min + 1 only when none is admissible); appends are warp-collective
+      auto thread_discharge = [&](bool thr, int u, const Seg& sg, int d, int hu, long long eu, const QueueOut& oq,
+                                  unsigned long long& wk) {
+        unsigned long long best = ~0ull;
+        long long budget = eu, pushed = 0;
+        int scanned = 0;
+        for (int b0 = 0; __any_sync(FULL, thr && b0 < d && budget > 0); b0 += 8) {
+          const bool act = thr && b0 < d && budget > 0;
+          int col[8], cf[8], sl[8];
+          if constexpr (Ops::kVec8) {
+            if (act) ops.arcs8(sg, b0, d, col, cf);
+            else {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) { col[j] = 0; cf[j] = 0; }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) sl[j] = sg.fb + b0 + j;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              col[j] = 0; cf[j] = 0; sl[j] = 0;
+              if (act && b0 + j < d) ops.out_arc(sg, b0 + j, col[j], cf[j], sl[j]);
+            }
+          }
+          if (act) scanned += min(8, d - b0);
+          int hv[8], ax[8], dg[8];
+          uint8_t tm[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            hv[j] = cf[j] > 0 ? ld_h(P.h + col[j], pl) : INT_MAX;
+            ax[j] = cf[j] > 0 ? ops.aux(sl[j]) : 0;
+            dg[j] = cf[j] > 0 ? ops.degree(col[j]) : 0;
+            tm[j] = cf[j] > 0 ? ld_term(P.term + col[j]) : 1;
+          }
+          bool app[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            app[j] = false;
+            if (cf[j] > 0) {
+              const unsigned long long cand = ((unsigned long long)(unsigned)hv[j] << 32) | (unsigned)sl[j];
+              if (cand < best) best = cand;
+            }
+            if (cf[j] > 0 && hv[j] < hu && budget > 0) {
+              const int dd = (int)(budget < (long long)cf[j] ? budget : (long long)cf[j]);
+              ops.push_aux(sl[j], ax[j], dd);
+              const long long old_v = (long long)atomicAdd((unsigned long long*)(P.e + col[j]), (unsigned long long)dd);
+              app[j] = old_v == 0 && tm[j] == 0;
+              budget -= dd;
+              pushed += dd;
+              ++st_push;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const bool hg = app[j] && dg[j] > kRChunk;
+            if (hg) huge_append(col[j], dg[j], oq, kRChunk);
+            warp_append(S, cnt, app[j] && !hg, col[j], oq, dg[j]);
+          }
         }
+        st_arcs += scanned;
+        bool app_u = false;
+        if (thr) {
+          if (pushed > 0) {
+            const long long old_u = (long long)atomicAdd((unsigned long long*)(P.e + u), (unsigned long long)(-pushed));
+            app_u = old_u - pushed > 0;
+          } else {
+            const unsigned hmin = (unsigned)(best >> 32);
+            const int nh = (best == ~0ull || (int)hmin >= N - 1) ? N : (int)hmin + 1;
+            st_cg(P.h + u, nh);
+            gap_relabel(hu, nh);
+            app_u = nh < N;
+            wk += (unsigned long long)d + 1;
+            ++st_relabel;
+          }
+        }
+        warp_append(S, cnt, app_u, u, oq, d);
+      };
+      // one task: vertex u, or chunk [lo, lo + kRChunk) of hub record hidx (the whole warp)
+      auto run_task = [&](int u, int lo, int hidx) {
         // independent loads issued together: segment bounds, h(u), e(u)
         Seg sg = ops.seg(u);
         const int hu = ld_cg(P.h + u);
         const long long eu = ld_cg(P.e + u);
-        if (hu >= N) continue;   // lifted by the gap heuristic: inactive until the next GR
+        if (hu >= N) return;     // lifted by the gap heuristic: inactive until the next GR
+        int hi;
         if (hidx < 0) { lo = 0; hi = sg.deg(); } else { hi = min(sg.deg(), lo + kRChunk); }
         if (lane == 0) st_arcs += hi - lo;
 
@@ -1525,7 +1596,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               if (wbest != ~0ull) ops.col_cf_of_slot((int)(wbest & 0xffffffffu), colv, cfv);
             }
           }
-          if (!__shfl_sync(FULL, last, 0)) continue;
+          if (!__shfl_sync(FULL, last, 0)) return;
           wbest = __shfl_sync(FULL, wbest, 0);
           colv = __shfl_sync(FULL, colv, 0);
           cfv = __shfl_sync(FULL, cfv, 0);
@@ -1563,6 +1634,55 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         }
         warp_append(S, cnt, lane == 0 && app_u >= 0, app_u, o, dgu);
         warp_append(S, cnt, lane == 0 && app_v >= 0, app_v, o, dgv);
+      };
+      // many active vertices (e.g. the first rounds of a matching, ~10^6 of them): 32 queue
+      // entries per warp, those with <= kRThr slots discharged by one THREAD each (8-slot
+      // batches, all loads of a batch in flight together), the rest by the whole warp
+      // (only when no queued vertex has more than kRThr slots: a warp that met big vertices among
+      //  its 32 entries would run them one after another - skewed graphs keep the warp mode)
+      const bool thread_mode = P.push_mode != 0 && qn >= nwarps * kRThrPack && hc == 0 && (S.bc.flags & 64);
+      if (thread_mode) {
+        for (int t = gwarp; t < hc; t += nwarps) {
+          ++tn0;
+          const int2 c = ld_cg(hcc + t);
+          run_task(ld_cg(&hqc[c.x].u), c.y * kRChunk, c.x);
+        }
+        for (int base = gwarp * 32; base < qn; base += nwarps * 32) {
+          ++tn0;
+          const int tk = base + lane;
+          const int u = tk < qn ? ld_cg(qc + tk) : -1;
+          Seg sg;
+          sg.fb = sg.fe = sg.rb = sg.re = 0;
+          int hu = N;
+          long long eu = 0;
+          if (u >= 0) { sg = ops.seg(u); hu = ld_cg(P.h + u); eu = ld_cg(P.e + u); }
+          const int d = sg.deg();
+          const bool thr = u >= 0 && hu < N && d <= kRThr;
+          thread_discharge(thr, u, sg, d, hu, eu, o, work);
+          unsigned todo = __ballot_sync(FULL, u >= 0 && hu < N && !thr);
+          while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            run_task(__shfl_sync(FULL, u, j), 0, -1);
+          }
+        }
+      } else {
+      // the queue entry of a warp's next task is loaded while the current one runs
+      int u_next = gwarp < qn ? ld_cg(qc + gwarp) : 0;
+      for (int tk = gwarp; tk < total; tk += nwarps) {
+        ++tn0;
+        int u, lo = 0, hidx = -1;
+        if (tk < qn) {
+          u = u_next;
+          if (tk + nwarps < qn) u_next = ld_cg(qc + tk + nwarps);
+        } else {
+          int2 c = ld_cg(hcc + (tk - qn));
+          hidx = c.x;
+          lo = c.y * kRChunk;
+          u = ld_cg(&hqc[hidx].u);
+        }
+        run_task(u, lo, hidx);
+      }
       }
       trace_end(tt0, ta0, tp0, tr0c, tn0);
       ++trace_round;

@@ -21,8 +21,13 @@ if a.cfg == "c5":
     for _ in range(2):
         _, _, _, st = W.maxflow_batch(ro, col, cap, B.vbase, B.s, B.t, workspace=ws, **opt)
 else:
+    def c4():
+        from oracle import matching
+        l, r = synth.bipartite_edges()
+        n, src, dst, cap, s_, t_ = matching.network(1 << 20, 1 << 20, l, r)
+        return synth.from_edges(n, src, dst, cap, s_, t_)
     g = {"r18h": lambda: synth.rmat(18, 16, 1000, "hub20"), "c3h": lambda: synth.rmat(22, 16, 1, "hub20"),
-         "c3p": lambda: synth.rmat(22, 16, 1, "paper")}[a.cfg]()
+         "c3p": lambda: synth.rmat(22, 16, 1, "paper"), "c4": c4}[a.cfg]()
     ro, col, cap = (torch.from_numpy(x).cuda() for x in (g.row_off, g.col, g.cap))
     ws = W.Workspace(W.workspace_size(g.n, g.m, 1, W.options("bcsr", **opt)))
     for _ in range(2):
