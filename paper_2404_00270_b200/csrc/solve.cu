@@ -211,7 +211,10 @@ constexpr int kAsyncLevel = 32;   // bfs_mode 3: a GR deeper than this continues
 #ifndef WBPR_ASYNC_WARPS
 #define WBPR_ASYNC_WARPS 128         // warps taking part in the asynchronous GR continuation (best of 128/512/2048)
 #endif
-constexpr int kTdThread = 8;      // top-down BFS: frontier vertices up to this many slots are scanned by one thread
+#ifndef WBPR_TDT
+#define WBPR_TDT 8
+#endif
+constexpr int kTdThread = WBPR_TDT; // top-down BFS: frontier vertices up to this many slots are scanned by one thread
 constexpr int kTdPack = 4;        // top-down BFS: pack 32 frontier entries per warp when |frontier| >= kTdPack x warps
 #ifndef WBPR_RU
 #define WBPR_RU 4
