@@ -514,15 +514,11 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
   // ---------------------------------------------------------------- preflow (Alg. 1 Step 0)
   {
     unsigned long long exc = 0;
-    // many instances: one CTA per source (in turn); few: the whole grid on each source's arcs
-    const bool per_cta = KI >= (int)nb / 4;
-    for (int i = I0 + (per_cta ? brank : 0); i < I0 + KI; i += per_cta ? (int)nb : 1) {
+    for (int i = I0; i < I0 + KI; ++i) {
       int s = (int)P.src[i];
       Seg sg = ops.seg(s);
       int d = sg.deg();
-      const int j0 = per_cta ? (int)threadIdx.x : brank * (int)blockDim.x + (int)threadIdx.x;
-      const int js = per_cta ? (int)blockDim.x : (int)(nb * blockDim.x);
-      for (int j = j0; j < d; j += js) {
+      for (int j = brank * blockDim.x + threadIdx.x; j < d; j += nb * blockDim.x) {
         int col, cf, slot;
         ops.out_arc(sg, j, col, cf, slot);
         if (cf > 0) {   // c_f(s,v) <- 0, c_f(v,s) <- c(s,v), e(v) <- c(s,v)
