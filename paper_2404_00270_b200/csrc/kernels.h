@@ -71,8 +71,14 @@ void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st)
 // solve.cu
 int solve_max_blocks_per_sm(int layout, int threads);
 cudaError_t launch_solve(const SolveParams& p, int blocks, int threads, cudaStream_t st);
-constexpr int kSolveThreads = 512;
-constexpr int kSolveMinBlocks = 2;   // default register budget of k_solve (see solve.cu)
+#ifndef WBPR_SOLVE_THREADS
+#define WBPR_SOLVE_THREADS 512
+#endif
+#ifndef WBPR_SOLVE_MINB_DEFAULT
+#define WBPR_SOLVE_MINB_DEFAULT 2
+#endif
+constexpr int kSolveThreads = WBPR_SOLVE_THREADS;
+constexpr int kSolveMinBlocks = WBPR_SOLVE_MINB_DEFAULT;   // default register budget of k_solve (see solve.cu)
 
 // extract.cu
 void extract_results(const SolveParams& p, const int64_t* ro, const int32_t* col, const int32_t* cap,

@@ -1761,7 +1761,7 @@ static int solve_minb() {
 }
 
 template <class Ops> static const void* solve_fn() {
-  return solve_minb() == 1 ? (const void*)k_solve<Ops, 1> : (const void*)k_solve<Ops, 2>;
+  return solve_minb() == 1 ? (const void*)k_solve<Ops, 1> : (const void*)k_solve<Ops, kSolveMinBlocks>;
 }
 
 int solve_max_blocks_per_sm(int layout, int threads) {
