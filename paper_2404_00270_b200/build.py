@@ -11,6 +11,7 @@ from __future__ import annotations
 import concurrent.futures as cf
 import hashlib
 import os
+import re
 import subprocess
 import sys
 
@@ -39,7 +40,7 @@ def _digest() -> str:
     for p in _sources() + _headers():
         with open(p, "rb") as f:
             h.update(p.encode() + f.read())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    h.update(" ".join(ARCH + FLAGS + ["-Xptxas", "-v", "ptxas-report"]).encode())
     return h.hexdigest()
 
 
@@ -56,10 +57,12 @@ def build(force: bool = False, verbose: bool = False, defines=(), variant: str =
 
     def comp(src):
         obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
-        cmd = [NVCC] + ARCH + FLAGS + list(defines) + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+        cmd = [NVCC] + ARCH + FLAGS + list(defines) + ["-Xptxas", "-v", "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        with open(obj + ".ptxas.txt", "w") as f:   # register / spill report, see ptxas_report()
+            f.write(r.stderr)
         return obj, r.stderr
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
@@ -75,6 +78,28 @@ def build(force: bool = False, verbose: bool = False, defines=(), variant: str =
     os.replace(tmp, out)
     with open(stamp, "w") as f:
         f.write(dg)
+    return out
+
+
+def ptxas_report(source: str = "solve.cu", variant: str = "") -> dict:
+    """{mangled kernel name: (registers, spill store bytes, spill load bytes)} from the ptxas
+    report the last build of `source` left next to its object file."""
+    obj_dir = OBJ if not variant else os.path.join(OBJ, variant)
+    txt = open(os.path.join(obj_dir, source + ".o.ptxas.txt")).read()
+    out, name, spill = {}, None, (0, 0)
+    for line in txt.splitlines():
+        m = re.search(r"Compiling entry function '(\w+)'", line)
+        if m:
+            name, spill = m.group(1), (0, 0)
+            continue
+        m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
+        if m and name:
+            spill = (int(m.group(1)), int(m.group(2)))
+            continue
+        m = re.search(r"Used (\d+) registers", line)
+        if m and name:
+            out[name] = (int(m.group(1)),) + spill
+            name = None
     return out
 
 

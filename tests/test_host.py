@@ -103,3 +103,22 @@ def test_gather_records_gloo_world2():
     assert got[:, 0].tolist() == list(range(6))
     for i in range(6):
         assert got[i, 2] == oracle.maxflow_graph(synth.rmat(9, 8, 500 + i, "paper"), phase2=False).flow
+
+
+def test_solve_register_budget():
+    """k_solve's register budget is a measured performance property: a change that raised the
+    default instantiation's spills from 2536 to ~2620 B of stores (24 -> 80 B in the 128-register
+    one) cost 12 % on C5.  Guard the ptxas report of the current build."""
+    from paper_2404_00270_b200 import build as B
+    B.build()
+    rep = B.ptxas_report("solve.cu")
+    budget = {   # (registers, max spill-store bytes) per instantiation, as measured
+        "_ZN4wbpr7k_solveINS_7BcsrOpsELi2EEEvNS_11SolveParamsET_": (64, 2560),
+        "_ZN4wbpr7k_solveINS_7BcsrOpsELi1EEEvNS_11SolveParamsET_": (128, 48),
+        "_ZN4wbpr7k_solveINS_7RcsrOpsELi2EEEvNS_11SolveParamsET_": (64, 3200),
+        "_ZN4wbpr7k_solveINS_7RcsrOpsELi1EEEvNS_11SolveParamsET_": (128, 512),
+    }
+    for name, (regs, spill) in budget.items():
+        assert name in rep, name
+        r, st, _ = rep[name]
+        assert r <= regs and st <= spill, (name, rep[name])
