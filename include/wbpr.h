@@ -23,8 +23,15 @@
  *     process.  wbpr_last_error() returns a message for the last failure on the
  *     calling thread.
  *   - Synchronous: work is enqueued on `stream` (a cudaStream_t passed as void*,
- *     NULL = legacy default stream), the call synchronises the stream once at the
- *     end, and results are valid on return.
+ *     NULL = legacy default stream) and results are valid on return.  A BCSR solve
+ *     synchronises the stream twice: once after the validation kernels (so a
+ *     malformed graph is reported before construction) and once at the end; RCSR
+ *     adds two more (its reverse sort is sized from device counts), batch_groups > 1
+ *     one more.  On every error return after work was enqueued the stream is
+ *     synchronised first, so the caller may free or reuse the workspace at once.
+ *   - Host staging: small copies (terminals, instance ranges, results) go through a
+ *     per-thread pinned buffer that only grows (never freed while the thread lives),
+ *     so a solve never calls cudaFreeHost.
  *   - Ownership: inputs are never written; the workspace is caller-allocated
  *     device memory of at least wbpr_*_workspace_size() bytes (256-B aligned);
  *     the library performs no cudaMalloc inside a solve.  One workspace serves
@@ -123,6 +130,13 @@ typedef struct wbpr_options {
                             union (it shares the grid dynamically: on C5 the groups' static
                             CTA shares leave the easy groups' CTAs idle behind the hardest
                             instance, profiles/r1)                                           */
+  int32_t debug_stop;    /* testing (single instance, phase 1): > 0 stops the solve right after
+                            the active-vertex compaction that follows the debug_stop-th global
+                            relabel.  h[] then holds that GR's exact labels (distance to t in
+                            G_f, unreached = n), e[] the excess, and the residual
+                            view exposes the compacted AVQ (Alg. 2 l.1-4).  The
+                            flow value is not final and the certificate is not checked.
+                            0 (default): off                                                 */
 } wbpr_options;
 
 typedef struct wbpr_stats {
@@ -152,6 +166,9 @@ typedef struct wbpr_stats {
                                 6 gap lifts, 7 asynchronous GR continuation, 8 bottom-up
                                 BFS levels, 9 small-frontier spans                          */
   int64_t phase_count[10];   /* phases per kind (small-frontier: phases run in CTA mode)  */
+  int64_t bfs_arcs_bottom_up; /* the part of bfs_arcs_scanned read by bottom-up levels (a
+                                 slot's own {col, cf} + h[col]: 12 B); the rest are top-down
+                                 in-arcs (col, mate, cf[mate], h: 16 B) - DESIGN.md §5      */
 } wbpr_stats;
 
 /* Fill *opt with the defaults above. */
@@ -225,6 +242,10 @@ typedef struct wbpr_residual {
   const int64_t* e;
   const int32_t* h;
   const int32_t* seg;   /* BCSR: int2 {begin, end} per vertex [n] (gapped segments) */
+  const int32_t* avq;   /* debug_stop solves: the compacted active-vertex queue [avq_len]
+                           (normal entries, then one entry per hub vertex); else NULL */
+  int64_t avq_len;
+  int64_t excess_total; /* Excess_total after the last compaction          */
 } wbpr_residual;
 wbpr_status wbpr_residual_view(const void* workspace, wbpr_residual* view);
 
@@ -239,6 +260,15 @@ wbpr_status wbpr_build_residual(const wbpr_csr* g, const wbpr_options* opt, void
  * int slots, int pushes, int relabels, int schedule} laid out [round][warp];
  * *rounds = traced rounds, *warps = warps of the persistent grid. */
 wbpr_status wbpr_trace_view(const void* workspace, const void** records, int64_t* rounds, int32_t* warps);
+
+/* Measurement helper (not part of a solve): the device time of one EMPTY grid-synchronous
+ * phase of the persistent solve kernel - the same barrier protocol (one acq_rel arrival per
+ * CTA, last-arriver bookkeeping, one 16-B release store, acquire polling) with no work in
+ * between, on grid_blocks co-resident CTAs (0 = the full persistent grid), averaged over
+ * `iters` phases.  phases x this cost is the latency floor of a solve (the paper's
+ * synchronisation overhead on small / long-path graphs).
+ * Synchronises `stream`; may allocate 8 B of device memory.  Errors: EINVAL, ECUDA. */
+wbpr_status wbpr_barrier_cost(int32_t grid_blocks, int32_t iters, double* ns_per_phase, void* stream);
 
 const char* wbpr_status_string(wbpr_status st);
 const char* wbpr_last_error(void);

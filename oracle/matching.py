@@ -30,7 +30,13 @@ def check_matching(nL, nR, l, r, match_of_left, size):
     assert np.all(used < nR), "right id out of range"
     assert np.unique(used).shape[0] == used.shape[0], "a right vertex is matched twice"
     assert used.shape[0] == size, f"matching has {used.shape[0]} pairs, expected {size}"
-    edges = set(zip(np.asarray(l).tolist(), np.asarray(r).tolist()))
-    for li in np.nonzero(m >= 0)[0].tolist():
-        assert (li, int(m[li])) in edges, f"pair ({li},{int(m[li])}) is not an input edge"
+    # every pair is an input edge: membership of l * nR + r in the sorted edge keys
+    keys = np.unique(np.asarray(l, np.int64) * nR + np.asarray(r, np.int64))
+    li = np.nonzero(m >= 0)[0]
+    q = li * nR + m[li]
+    pos = np.minimum(np.searchsorted(keys, q), max(keys.shape[0] - 1, 0))
+    hit = keys[pos] == q if keys.shape[0] else np.zeros(q.shape[0], bool)
+    if not np.all(hit):
+        j = int(li[np.nonzero(~hit)[0][0]])
+        raise AssertionError(f"pair ({j},{int(m[j])}) is not an input edge")
     return True

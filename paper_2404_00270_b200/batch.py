@@ -17,6 +17,27 @@ def partition(total: int, world: int, rank: int):
     return lo, hi
 
 
+def partition_weighted(weights, world: int, rank: int):
+    """Contiguous block [lo, hi) of instance ids for `rank`, balanced by weight (the edge
+    count m of every instance): boundary r sits where the running weight is
+    closest to r/world of the total, every rank keeping at least one instance when there
+    are enough of them."""
+    w = np.asarray(weights, np.float64)
+    total = w.shape[0]
+    if world <= 1 or total == 0:
+        return (0, total) if rank == 0 else (total, total)
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    cuts = [0]
+    for r in range(1, world):
+        target = cum[-1] * r / world
+        i = int(np.argmin(np.abs(cum - target)))
+        lo_ok = cuts[-1] + (1 if total >= world else 0)       # at least one per rank
+        hi_ok = total - (world - r if total >= world else 0)  # leave one for each later rank
+        cuts.append(int(min(max(i, lo_ok), hi_ok)))
+    cuts.append(total)
+    return cuts[rank], cuts[rank + 1]
+
+
 def make_records(ids, flows, cuts, stats=None, status=0) -> np.ndarray:
     """int64[k, 8] records (64 B each)."""
     k = len(ids)
@@ -35,13 +56,21 @@ def make_records(ids, flows, cuts, stats=None, status=0) -> np.ndarray:
 
 def gather_records(local, total: int, world: int, device=None):
     """All-gather every rank's records; returns int64[total, 8] ordered by instance id.
-    `local` is a torch int64 tensor [k_local, 8] on the collective's device."""
+    `local` is a torch int64 tensor [k_local, 8] on the collective's device.  When a
+    process group is initialised the collective runs at every world size (world 1 too)."""
     import torch
     import torch.distributed as dist
-    if world == 1:
+    if world == 1 and not (dist.is_available() and dist.is_initialized()):
         out = local
     else:
-        cap = -(-total // world)   # pad every rank to the same row count
+        cap = -(-total // world) if world > 0 else total
+        cap = max(cap, int(local.shape[0]))
+        # ranks may own different counts (weighted partition): pad to the largest
+        if world > 1:
+            n_local = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+            sizes = [torch.empty_like(n_local) for _ in range(world)]
+            dist.all_gather(sizes, n_local)
+            cap = max(int(s.item()) for s in sizes)
         buf = torch.full((cap, local.shape[1]), -1, dtype=torch.int64, device=local.device)
         buf[:local.shape[0]] = local
         parts = [torch.empty_like(buf) for _ in range(world)]

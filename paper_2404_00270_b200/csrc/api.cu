@@ -89,17 +89,30 @@ struct Ws {
 // group descriptors, the control record, per-instance results).  Pageable copies are staged
 // by the driver and can serialise with other streams' transfers, which would stop one
 // caller thread's large H2D from overlapping another thread's kernels.  One buffer per host
-// thread, grown on demand; every call synchronises its stream before returning, so a region
-// is never reused while a copy from / to it is in flight.
+// thread; every call synchronises its stream before returning, so a region is never reused
+// while a copy from / to it is in flight.  The first allocation covers every group descriptor
+// and a few thousand instances; a larger request allocates a bigger buffer and RETIRES the old
+// one (kept until the thread exits): cudaFreeHost synchronises the whole device and would
+// stall other threads' streams in the middle of their solves.
 struct PinnedScratch {
   char* p = nullptr;
   size_t cap = 0;
-  ~PinnedScratch() { if (p) cudaFreeHost(p); }
+  std::vector<char*> retired;
+  ~PinnedScratch() {
+    if (p) cudaFreeHost(p);
+    for (char* r : retired) cudaFreeHost(r);
+  }
   char* get(size_t n) {
     if (n > cap) {
-      if (p) cudaFreeHost(p);
-      cap = std::max<size_t>(n, size_t(1) << 16);
-      if (cudaHostAlloc(reinterpret_cast<void**>(&p), cap, cudaHostAllocPortable) != cudaSuccess) { p = nullptr; cap = 0; }
+      const size_t want = std::max<size_t>(n, sizeof(GroupDesc) * kMaxGroups + sizeof(Ctrl) + (size_t(1) << 17));
+      char* q = nullptr;
+      if (cudaHostAlloc(reinterpret_cast<void**>(&q), want, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;   // callers fall back to pageable copies
+      }
+      if (p) retired.push_back(p);
+      p = q;
+      cap = want;
     }
     return p;
   }
@@ -241,6 +254,14 @@ wbpr_status check_graph_args(const wbpr_csr* g) {
   return WBPR_OK;
 }
 
+// Every error return after work was enqueued on the stream synchronises it first (the
+// persistent kernel may still be writing the caller's workspace).
+struct SyncOnExit {
+  cudaStream_t st;
+  bool armed = false;
+  ~SyncOnExit() { if (armed) { cudaStreamSynchronize(st); cudaGetLastError(); } }
+};
+
 struct Events {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   ~Events() { for (auto& e : ev) if (e) cudaEventDestroy(e); }
@@ -281,9 +302,14 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   const Layout& L = W.L;
 
   if (opt.batch_groups < 0) return fail(WBPR_EINVAL, "batch_groups must be >= 0");
+  if (opt.debug_stop < 0) return fail(WBPR_EINVAL, "debug_stop must be >= 0");
+  if (opt.debug_stop > 0 && (k != 1 || opt.phase2 || opt.schedule != 0))
+    return fail(WBPR_EINVAL, "debug_stop needs a single-instance vertex-centric phase-1 solve");
   const long long launches0 = launch_count();
   Events E;
   CK(E.create());
+  SyncOnExit guard{st};
+  guard.armed = true;
   CK(cudaEventRecord(E.ev[0], st));
 
   const int64_t* ro = g->row_offsets;
@@ -372,6 +398,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   P.h1 = at<int>(ws, L.h1);
   P.gr_gamma = opt.gr_gamma;
   P.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
+  P.debug_stop = opt.debug_stop;
   int occ = di.occ[opt.layout];
   if (occ < 1) return fail(WBPR_ECUDA, "solve kernel cannot be resident on this device");
   int blocks = di.num_sms * occ;
@@ -517,6 +544,7 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   if (pin) CK(cudaMemcpyAsync(pin, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   else CK(cudaMemcpyAsync(&c, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  guard.armed = false;
   if (pin) {
     memcpy(&c, pin, sizeof(Ctrl));
     memcpy(hf.data(), pin + sizeof(Ctrl), 8 * k);
@@ -525,6 +553,13 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
 
   const int M = opt.layout == WBPR_LAYOUT_BCSR ? c.M : 2 * Mf;
   register_view(W, opt.layout, M, opt.layout == WBPR_LAYOUT_BCSR ? c.M : Mf);
+  if (opt.debug_stop > 0) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    wbpr_residual& v = g_views[W.base];
+    v.avq = at<int32_t>(ws, L.q0);
+    v.avq_len = (int64_t)c.dbg_qn + c.dbg_hn;
+    v.excess_total = c.excess_total;
+  }
   if (c.overflow == 1) return fail(WBPR_EOVERFLOW, "merged capacity exceeds INT32_MAX");
   if (c.overflow == 2) return fail(WBPR_EINTERNAL, "reverse arc not found while building mate[]");
   long long F = 0, C = 0;
@@ -563,9 +598,11 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
     stats->t_flush_ns = c.stats[ST_COUNT - 2];
     stats->t_round_ns = c.stats[ST_COUNT - 1];
     for (int i = 0; i < kPhBuckets; ++i) { stats->phase_ns[i] = c.phase_ns[i]; stats->phase_count[i] = c.phase_cnt[i]; }
+    stats->bfs_arcs_bottom_up = c.stats[ST_BFS_BU];
   }
   if (c.status == DS_NOTCONVERGED) return fail(WBPR_ENOTCONVERGED, "round cap exceeded");
   if (c.abort) return fail(WBPR_ENOTCONVERGED, "device watchdog timeout");
+  if (opt.debug_stop > 0) return WBPR_OK;   // stopped mid-solve: no certificate (wbpr.h)
   if (!cert) return fail(WBPR_EINTERNAL, "certificate failed: cut capacity != flow value");
   // Paper's termination identity: e(s) + e(t) >= Excess_total at the end.
   if (F != c.excess_total) return fail(WBPR_EINTERNAL, "Excess_total bookkeeping disagrees with e(t)");
@@ -709,6 +746,17 @@ wbpr_status wbpr_trace_view(const void* workspace, const void** records, int64_t
   *records = it->second.ptr;
   *rounds = it->second.rounds;
   *warps = it->second.warps;
+  return WBPR_OK;
+}
+
+wbpr_status wbpr_barrier_cost(int32_t grid_blocks, int32_t iters, double* ns_per_phase, void* stream) {
+  if (!ns_per_phase || iters < 1) return fail(WBPR_EINVAL, "bad arguments");
+  DevInfo di;
+  wbpr_status s = dev_info(di);
+  if (s) return s;
+  int blocks = di.num_sms * std::max(1, di.occ[0]);
+  if (grid_blocks > 0 && grid_blocks < blocks) blocks = grid_blocks;
+  CK(barrier_probe(blocks, iters, ns_per_phase, (cudaStream_t)stream));
   return WBPR_OK;
 }
 

@@ -181,7 +181,7 @@ __global__ void k_merge_write(const uint64_t* __restrict__ keys, int64_t H, cons
 constexpr int kMatePerThread = 4;
 __global__ void __launch_bounds__(256) k_mate(const int* __restrict__ ine, const int* __restrict__ inslot,
                                               const int* __restrict__ outslot, const int* __restrict__ rsoff, int n,
-                                              int* mate) {
+                                              int* mate, const int* __restrict__ cap0, Ctrl* ctrl) {
   const int total = __ldg(rsoff + n);   // in-list entries
   const int base = blockIdx.x * blockDim.x * kMatePerThread + threadIdx.x;
   int e[kMatePerThread], q[kMatePerThread];
@@ -197,6 +197,15 @@ __global__ void __launch_bounds__(256) k_mate(const int* __restrict__ ine, const
 #pragma unroll
   for (int r = 0; r < kMatePerThread; ++r)
     if (p[r] >= 0) { mate[q[r]] = p[r]; mate[p[r]] = q[r]; }
+  // the pair's residual capacities sum to cap0[p] + cap0[q] forever (a push moves d between
+  // them): beyond INT32_MAX the int32 cf would wrap, so report EOVERFLOW.  Only checked when
+  // the merge saw a capacity above INT32_MAX / 2 (otherwise no pair can exceed it).
+  if (ld_cg(&ctrl->bigcap)) {
+#pragma unroll
+    for (int r = 0; r < kMatePerThread; ++r)
+      if (p[r] >= 0 && (long long)__ldg(cap0 + p[r]) + (long long)__ldg(cap0 + q[r]) > INT_MAX)
+        atomicExch(&ctrl->overflow, 1);
+  }
 }
 
 // RCSR reverse in-degree over forward arcs
@@ -265,7 +274,7 @@ void build_bcsr_mate(const BuildArgs& a, cudaStream_t st) {
   const int T = 256;
   // one thread per kMatePerThread in-list entries (rsoff[n] of them; m bounds it)
   const int64_t per_block = (int64_t)T * kMatePerThread;
-  if (a.m > 0) { k_mate<<<(unsigned)((a.m + per_block - 1) / per_block), T, 0, st>>>(a.ine, a.inslot, a.outslot, a.rsoff, (int)a.n, a.mate); note_launch(); }
+  if (a.m > 0) { k_mate<<<(unsigned)((a.m + per_block - 1) / per_block), T, 0, st>>>(a.ine, a.inslot, a.outslot, a.rsoff, (int)a.n, a.mate, a.cap0, a.ctrl); note_launch(); }
 }
 
 void k_ro_to_i32_ext(const int64_t* ro, int64_t n, int* out, int num_sms, cudaStream_t st) {

@@ -83,7 +83,9 @@ struct HugeRec {
 
 enum StatIdx {
   ST_ROUNDS = 0, ST_GRS, ST_BFS_LEVELS, ST_PUSHES, ST_RELABELS, ST_ARCS, ST_BFS_ARCS,
-  ST_CAND, ST_AVQ, ST_GAPLIFT, ST_SMALL_PHASES, ST_SMALL_ENTRIES, ST_COUNT = 16
+  ST_CAND, ST_AVQ, ST_GAPLIFT, ST_SMALL_PHASES, ST_SMALL_ENTRIES,
+  ST_BFS_BU,   // residual slots read by bottom-up BFS levels (ST_BFS_ARCS counts both directions)
+  ST_COUNT = 16
 };
 
 enum DevStatus { DS_OK = 0, DS_NOTCONVERGED = 1, DS_TIMEOUT = 2, DS_INTERNAL = 3 };
@@ -150,6 +152,8 @@ struct Ctrl {
   int mlist_w, mlist_c;   // build: vertices merged by a warp / by a CTA
   int maxlen_out;         // build: longest input row
   int any_unsorted;       // build: some input row is not column-sorted (else the row sort is skipped)
+  int bigcap;             // build: some merged BCSR capacity exceeds INT32_MAX / 2 (pair-sum check needed)
+  int dbg_qn, dbg_hn;     // debug_stop: AVQ entries / hub vertices exported after the stopping GR
   long long phase_ns[kPhBuckets];    // solve: barrier-release-to-release time per phase kind
   long long phase_cnt[kPhBuckets];
 };
@@ -260,6 +264,8 @@ struct SolveParams {
   int small_mode;        // 1: phases with small queues run in CTA 0 alone (thread per vertex)
   int schedule;          // 0: vertex-centric (AVQ + warp per vertex, Alg. 2); 1: thread-centric sweeps (Alg. 1)
   unsigned long long deadline_ns_rel;
+  int debug_stop;        // > 0: stop right after the compaction that follows the debug_stop-th
+                         // global relabel and export the AVQ (tests of the GR labels / AVQ)
 };
 
 }  // namespace wbpr

@@ -71,6 +71,7 @@ void build_rcsr_reverse(const BuildArgs& a, int Mf, int maxlen, cudaStream_t st)
 // solve.cu
 int solve_max_blocks_per_sm(int layout, int threads);
 cudaError_t launch_solve(const SolveParams& p, int blocks, int threads, cudaStream_t st);
+cudaError_t barrier_probe(int blocks, int iters, double* ns_per_barrier, cudaStream_t st);
 #ifndef WBPR_SOLVE_THREADS
 #define WBPR_SOLVE_THREADS 512
 #endif

@@ -112,6 +112,9 @@ struct MergeArgs {
 
 __device__ __forceinline__ void emit(const MergeArgs& a, int slot, uint32_t c, long long sum) {
   if (sum > INT_MAX) { atomicExch(&a.ctrl->overflow, 1); sum = INT_MAX; }
+  // a pair u->v / v->u shares one arc pair whose cf values always sum to cap0[p] + cap0[mate]
+  // (a push moves d from one to the other): flag big capacities so k_mate checks that sum
+  if (sum > (INT_MAX >> 1)) a.ctrl->bigcap = 1;
   a.arc[slot] = make_int2((int)c, (int)sum);
   a.cap0[slot] = (int)sum;
 }

@@ -743,6 +743,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
   int cur = 0, fb = 0;
   int state = S_GR;
   unsigned small_epoch = 0;
+  int grs_done = 0;       // global relabels started by this group (every thread; debug_stop)
 
   while (true) {
   while (state != S_DONE) {
@@ -881,6 +882,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
     }
 
     if (state == S_GR) {
+      ++grs_done;
       // ------------------------------------------------------------ global relabel
       // reset labels: sinks 0, everything else |V| (= unreached); frontier <- sinks
       {   // 4 independent vertices per thread and iteration (memory-level parallelism)
@@ -961,8 +963,17 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         if (pred) {
           const int pos = base + __popc(b & lanemask_lt());
           int2* const cell = aring + (pos % cap);
-          while (ld_acquire_v2(cell).x != pos) __nanosleep(20);
-          st_release_v2(cell, make_int2(pos + 1, v));
+          unsigned spins = 0;
+          bool ok = true;
+          while (ld_acquire_v2(cell).x != pos) {   // (the watchdog / abort word is polled here too)
+            __nanosleep(20);
+            if ((++spins & 255u) == 0 && (globaltimer() > deadline || ld_volatile(&C->abort))) {
+              atomicExch(&C->abort, 1);
+              ok = false;
+              break;
+            }
+          }
+          if (ok) st_release_v2(cell, make_int2(pos + 1, v));
         }
       };
       // seed: the frontier (normal entries and hub vertices, chunk 0 of each)
@@ -1016,10 +1027,22 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           const int pos = base + lane;
           int2* const cell = aring + (pos % cap);
           int2 c = ld_acquire_v2(cell);
-          while (c.x != pos + 1) { __nanosleep(20); c = ld_acquire_v2(cell); }
-          w = c.y;
-          st_release_v2(cell, make_int2(pos + cap, 0));
-          atom_exch_acquire(P.inq + w, 0);   // dequeued: a later improvement of h(w) re-queues it
+          unsigned spins = 0;
+          bool ok = true;
+          while (c.x != pos + 1) {
+            __nanosleep(20);
+            c = ld_acquire_v2(cell);
+            if ((++spins & 255u) == 0 && c.x != pos + 1 && (globaltimer() > deadline || ld_volatile(&C->abort))) {
+              atomicExch(&C->abort, 1);
+              ok = false;
+              break;
+            }
+          }
+          if (ok) {
+            w = c.y;
+            st_release_v2(cell, make_int2(pos + cap, 0));
+            atom_exch_acquire(P.inq + w, 0);   // dequeued: a later improvement of h(w) re-queues it
+          }
         }
         const int hw = w >= 0 ? ld_cg(P.h + w) : 0;
         Seg sw;
@@ -1150,6 +1173,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         } else {
           // ---- bottom-up: every unlabelled vertex v looks for an out-arc v -> w with
           // c_f > 0 and level(w) = level (early exit per 32-slot group)
+          unsigned long long bu = 0;   // slots read by this level (12 B each, §5; top-down 16 B)
           // the label / frozen flag of the next 32-vertex group are loaded one iteration ahead
           int nbase = VLO + gwarp * 32;
           int hv_next = nbase + lane < VHI ? ld_cg_hint(P.h + nbase + lane, pl) : -1;
@@ -1193,7 +1217,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
                 for (int j = 0; j < kBuB; ++j) self_hit |= hl[j] == level;
                 scanned += min(kBuB, dself - b0);
               }
-              st_bfs_arcs += scanned;   // per-thread partial; summed over the block at the end
+              bu += scanned;   // per-thread partial; summed over the block at the end
               if (self_hit) st_cg(P.h + v, level + 1);
             }
             unsigned todo = __ballot_sync(FULL, unl && !thr);
@@ -1209,7 +1233,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               if (d > kChunk) continue;            // hubs: static chunk tasks below
               int scanned = 0;
               const bool hit = bu_warp_scan(sg, 0, d, scanned);
-              if (lane == 0) st_bfs_arcs += scanned;
+              if (lane == 0) bu += scanned;
               if (hit) {
                 found_mask |= 1u << j;
                 if (lane == 0) st_cg(P.h + vv, level + 1);
@@ -1232,13 +1256,16 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
             int scanned = 0;
             const bool hit = bu_warp_scan(sg, lo2, hi2, scanned);
             if (lane == 0) {
-              st_bfs_arcs += scanned;
+              bu += scanned;
               if (hit && atomicCAS(P.h + vv, N, level + 1) == N) {
                 huge_append(vv, sg.deg(), o, kChunk);
                 fedges += sg.deg();
               }
             }
           }
+          st_bfs_arcs += bu;
+          const unsigned long long tb = block_sum_u64(S, bu);
+          if (threadIdx.x == 0 && tb) atomicAdd((unsigned long long*)&C->stats[ST_BFS_BU], tb);
         }
         {
           unsigned long long t = block_sum_u64(S, (unsigned long long)fedges);
@@ -1320,6 +1347,19 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       // termination: right after an exact GR, no active vertex <=> e(s)+e(t) >= Excess_total
       state = (S.bc.qn + S.bc.hc == 0) ? S_DONE : S_ROUND;
       if (state == S_DONE) converged = true;
+      if (P.debug_stop > 0 && grs_done >= P.debug_stop) {
+        // debug_stop: export the AVQ the compaction just built (entries, then one entry per hub
+        // vertex) and stop with the exact labels of this GR in h[] (tests of A3 / A5)
+        if (brank == 0) {
+          const int qn = S.bc.qn, hc = S.bc.hc;
+          for (int t = threadIdx.x; t < hc; t += blockDim.x) {
+            const int2 c = ld_cg(HC[0] + t);
+            if (c.y == 0) st_cg(Q[0] + qn + atomicAdd(&C->dbg_hn, 1), ld_cg(&HQ[0][c.x].u));
+          }
+          if (threadIdx.x == 0) C->dbg_qn = qn;
+        }
+        state = S_DONE;
+      }
       continue;
     }
 
@@ -1745,6 +1785,64 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       if (threadIdx.x == 0 && t) atomicAdd((unsigned long long*)&C->stats[idx[i]], t);
     }
   }
+}
+
+// ------------------------------------------------------------------ barrier-latency probe
+// The cost of one EMPTY grid-synchronous phase of k_solve (the latency floor of the
+// phase-bound workloads): the same arrival (one acq_rel atomic per
+// CTA), last-arriver bookkeeping (two 16-B ring loads + the abort word, one 16-B release
+// store) and acquire polling, with no work between barriers.  Same CTA size, co-resident grid.
+__device__ GroupCtrl g_probe_gc;
+__device__ int g_probe_abort;
+__global__ void __launch_bounds__(kSolveThreads, 1) k_barrier_probe(int iters, unsigned long long* out_ns) {
+  __shared__ uint4 sb;
+  GroupCtrl* GC = &g_probe_gc;
+  const unsigned nb = gridDim.x;
+  const unsigned long long t0 = globaltimer();
+  for (int it = 0; it < iters; ++it) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned target = (unsigned)it + 1;
+      uint4 b;
+      if (atom_add_acqrel(&GC->bar.count, 1u) == nb - 1) {
+        GC->bar.count = 0;
+        Ring* r = &GC->ring[it % 3];
+        const int4 r0 = ld_cg(reinterpret_cast<const int4*>(r));
+        const int4 r1 = ld_cg(reinterpret_cast<const int4*>(r) + 1);
+        const int ab = ld_volatile(&g_probe_abort);
+        b = make_uint4(target, (unsigned)(r0.x + r1.x), (unsigned)ab, 0u);
+        st_release_v4(&GC->bc, b);
+      } else {
+        unsigned ns = 0;
+        do {
+          b = ld_acquire_v4(&GC->bc);
+          if (b.x == target) break;
+          if (ns) __nanosleep(ns);
+          ns = ns ? (ns < 128 ? ns * 2 : 128) : 16;
+        } while (true);
+      }
+      sb = b;
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *out_ns = globaltimer() - t0;
+}
+
+cudaError_t barrier_probe(int blocks, int iters, double* ns_per_barrier, cudaStream_t st) {
+  GroupCtrl z{};
+  cudaError_t e = cudaMemcpyToSymbolAsync(g_probe_gc, &z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+  if (e) return e;
+  unsigned long long* d = nullptr;
+  if ((e = cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned long long), st))) return e;
+  void* args[] = {(void*)&iters, (void*)&d};
+  note_launch();
+  e = cudaLaunchCooperativeKernel((const void*)k_barrier_probe, dim3(blocks), dim3(kSolveThreads), args, 0, st);
+  unsigned long long ns = 0;
+  if (!e) e = cudaMemcpyAsync(&ns, d, sizeof(ns), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  if (!e) e = cudaStreamSynchronize(st);
+  if (!e) *ns_per_barrier = (double)ns / (double)(iters > 0 ? iters : 1);
+  return e;
 }
 
 // ------------------------------------------------------------------ host launch

@@ -24,7 +24,7 @@ _LAYOUTS = {"bcsr": 0, "rcsr": 1, 0: 0, 1: 1}
 EXPORTS = (
     "wbpr_default_options", "wbpr_workspace_size", "wbpr_maxflow_solve", "wbpr_maxflow_solve_batch",
     "wbpr_bipartite_workspace_size", "wbpr_bipartite_match", "wbpr_residual_view", "wbpr_build_residual",
-    "wbpr_status_string", "wbpr_last_error", "wbpr_version", "wbpr_trace_view",
+    "wbpr_status_string", "wbpr_last_error", "wbpr_version", "wbpr_trace_view", "wbpr_barrier_cost",
 )
 
 
@@ -45,7 +45,8 @@ class Options(ctypes.Structure):
                 ("max_rounds", ctypes.c_int64), ("grid_blocks", ctypes.c_int32), ("timeout_ms", ctypes.c_int32),
                 ("push_mode", ctypes.c_int32), ("gr_gamma", ctypes.c_float), ("l2_persist", ctypes.c_int32),
                 ("bfs_mode", ctypes.c_int32), ("small_mode", ctypes.c_int32), ("schedule", ctypes.c_int32),
-                ("phase2", ctypes.c_int32), ("trace_rounds", ctypes.c_int32), ("batch_groups", ctypes.c_int32)]
+                ("phase2", ctypes.c_int32), ("trace_rounds", ctypes.c_int32), ("batch_groups", ctypes.c_int32),
+                ("debug_stop", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -56,7 +57,8 @@ class Stats(ctypes.Structure):
         ("build_ms", ctypes.c_float), ("solve_ms", ctypes.c_float), ("extract_ms", ctypes.c_float),
         ("total_ms", ctypes.c_float), ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int64), ("t_barrier_ns", ctypes.c_int64), ("t_flush_ns", ctypes.c_int64),
-        ("t_round_ns", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 10), ("phase_count", ctypes.c_int64 * 10)]
+        ("t_round_ns", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 10), ("phase_count", ctypes.c_int64 * 10),
+        ("bfs_arcs_bottom_up", ctypes.c_int64)]
 
     def as_dict(self):
         d = {}
@@ -68,7 +70,8 @@ class Stats(ctypes.Structure):
 
 class Residual(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int32), ("n", ctypes.c_int64), ("M", ctypes.c_int64), ("Mf", ctypes.c_int64)] + [
-        (name, ctypes.c_void_p) for name in ("off", "arc", "mate", "cap0", "roff", "rarc", "bcf", "e", "h", "seg")]
+        (name, ctypes.c_void_p) for name in ("off", "arc", "mate", "cap0", "roff", "rarc", "bcf", "e", "h", "seg",
+                                             "avq")] + [("avq_len", ctypes.c_int64), ("excess_total", ctypes.c_int64)]
 
 
 _lib = None
@@ -104,6 +107,8 @@ def load():
     lib.wbpr_trace_view.argtypes = [P, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_int64),
                                     ctypes.POINTER(ctypes.c_int32)]
     lib.wbpr_trace_view.restype = ctypes.c_int32
+    lib.wbpr_barrier_cost.argtypes = [i32, i32, ctypes.POINTER(ctypes.c_double), P]
+    lib.wbpr_barrier_cost.restype = ctypes.c_int32
     lib.wbpr_status_string.argtypes = [i32]
     lib.wbpr_status_string.restype = ctypes.c_char_p
     lib.wbpr_last_error.restype = ctypes.c_char_p
@@ -123,7 +128,7 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
             l2_persist: Optional[int] = None, bfs_mode: Optional[int] = None,
             small_mode: Optional[int] = None, schedule: Optional[str] = None,
             phase2: Optional[int] = None, trace_rounds: Optional[int] = None,
-            batch_groups: Optional[int] = None) -> Options:
+            batch_groups: Optional[int] = None, debug_stop: Optional[int] = None) -> Options:
     o = Options()
     _check(load().wbpr_default_options(ctypes.byref(o)))
     o.layout = _LAYOUTS[layout]
@@ -152,6 +157,8 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
         o.trace_rounds = trace_rounds
     if batch_groups is not None:
         o.batch_groups = batch_groups
+    if debug_stop is not None:
+        o.debug_stop = debug_stop
     return o
 
 
@@ -315,6 +322,9 @@ def residual(workspace: Workspace) -> dict:
                    rcol=rarc[:, 0].copy(), fidx=rarc[:, 1].copy(), bcf=grab(v.bcf, v.Mf, torch.int32))
     out["e"] = grab(v.e, n, torch.int64)
     out["h"] = grab(v.h, n, torch.int32)
+    if v.avq:   # debug_stop solves: the compacted active-vertex queue and Excess_total
+        out["avq"] = grab(v.avq, v.avq_len, torch.int32)
+        out["excess_total"] = int(v.excess_total)
     return out
 
 
@@ -348,6 +358,17 @@ def trace(workspace: Workspace) -> np.ndarray:
     nbytes = rounds.value * warps.value * TRACE_DTYPE.itemsize
     raw = workspace.tensor[off:off + nbytes].cpu().numpy()
     return raw.view(TRACE_DTYPE).reshape(rounds.value, warps.value)
+
+
+def barrier_cost(grid_blocks: int = 0, iters: int = 2000, device=None) -> float:
+    """ns of device time per EMPTY grid-synchronous phase of the persistent solve kernel
+    (wbpr_barrier_cost): the latency floor per phase."""
+    torch = _torch()
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ns = ctypes.c_double()
+    with torch.cuda.device(dev):
+        _check(load().wbpr_barrier_cost(grid_blocks, iters, ctypes.byref(ns), _stream_ptr(dev)))
+    return float(ns.value)
 
 
 def version() -> str:

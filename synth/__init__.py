@@ -71,6 +71,18 @@ def _L():
             lib.synth_genrmf.restype = i64
             lib.synth_draw.argtypes = [u64, u64, u64]
             lib.synth_draw.restype = u64
+            lib.synth_set_threads.argtypes = [i32]
+            lib.synth_set_threads.restype = None
+            # (torchrun exports OMP_NUM_THREADS=1 to every rank: use this rank's share of the cores)
+            nt = os.environ.get("WBPR_SYNTH_THREADS")
+            if nt is None and os.environ.get("LOCAL_WORLD_SIZE"):
+                try:
+                    cores = len(os.sched_getaffinity(0))
+                except Exception:
+                    cores = os.cpu_count() or 1
+                nt = max(1, cores // int(os.environ["LOCAL_WORLD_SIZE"]))
+            if nt is not None:
+                lib.synth_set_threads(int(nt))
             _lib = lib
     return _lib
 
@@ -169,7 +181,7 @@ def rmat_edges(scale: int, edgefactor: int = 16, seed: int = 1):
     return src[:k].copy(), dst[:k].copy(), cap[:k].copy()
 
 
-def select_pairs(n, row_off, col, k=20, nstarts=128, seed=1):
+def select_pairs(n, row_off, col, k=20, nstarts=256, seed=1):
     srcs = np.empty(k, np.int32)
     snks = np.empty(k, np.int32)
     got = _L().synth_select_pairs(n, _p(row_off), _p(col), k, nstarts, seed, _p(srcs), _p(snks))
@@ -200,7 +212,7 @@ def add_super_terminals(n, src, dst, cap, sources, sinks):
 
 
 def rmat(scale: int = 22, edgefactor: int = 16, seed: int = 1, rule: str = "paper",
-         npairs: int = 20, nstarts: int = 128) -> Graph:
+         npairs: int = 20, nstarts: int = 256) -> Graph:
     """C3/C5: R-MAT instance with 20 source/sink pairs behind super terminals.
 
     rule="paper": BFS-chosen pairs with top-quartile depth (reading in

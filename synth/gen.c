@@ -24,6 +24,16 @@
 #include <omp.h>
 #endif
 
+/* Threads of the OpenMP regions (the draws are counter-based: results never depend on it).
+ * torchrun exports OMP_NUM_THREADS=1 to every rank; the bench sets its share of the cores. */
+void synth_set_threads(int32_t n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 static inline uint64_t mix64(uint64_t z) {
   z += 0x9E3779B97F4A7C15ull;
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

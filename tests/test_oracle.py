@@ -47,6 +47,42 @@ def test_spec_preflow_example(golden):
         assert tot == ex["excess_total"]
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_initial_state_vs_closed_form_and_library_bfs(seed):
+    """oracle.initial_state (Alg. 1 Step 0, then one reverse BFS from t)
+    against its closed form: e(v) = sum of c(s,v) over edges s->v (self-loops excluded),
+    Excess_total = their sum, and level = scipy's unweighted shortest-path distance to t on the
+    residual graph after the preflow (every arc out of s saturated, the reverse arcs v->s
+    holding c(s,v)); unreached vertices and s itself get n.  The CUDA path's first GR is
+    compared with these values bit-exactly (tests/test_gpu_state.py)."""
+    from scipy.sparse.csgraph import shortest_path
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(3, 40))
+    g = synth.tiny_random(n, int(rng.integers(0, 6 * n)), int(rng.integers(1, 9)), seed)
+    e, tot, lv, _ = oracle.initial_state(g.n, g.row_off, g.col, g.cap, g.s, g.t)
+    src, dst, cap = g.edges()
+    src = src.astype(np.int64); dst = dst.astype(np.int64); cap = cap.astype(np.int64)
+    keep = src != dst
+    src, dst, cap = src[keep], dst[keep], cap[keep]
+    from_s = src == g.s
+    want_e = np.bincount(dst[from_s], weights=cap[from_s], minlength=g.n).astype(np.int64)
+    want_e[g.s] = 0
+    assert np.array_equal(e, want_e) and tot == int(cap[from_s].sum())
+    # residual arcs after the preflow: forward u->v with c>0 unless u = s; backward v->u with
+    # the flow on (u,v), i.e. c(s,v) when u = s
+    fwd = (cap > 0) & ~from_s
+    bwd = from_s & (cap > 0)
+    a_src = np.concatenate([src[fwd], dst[bwd]])
+    a_dst = np.concatenate([dst[fwd], src[bwd]])
+    # distances TO t: BFS from t over reversed arcs; s is never expanded (P:159)
+    keep2 = a_dst != g.s   # a reversed arc out of s (an arc into s) would expand s
+    R = sp.csr_matrix((np.ones(int(keep2.sum())), (a_dst[keep2], a_src[keep2])), shape=(g.n, g.n))
+    d = shortest_path(R, method="D", unweighted=True, indices=g.t)
+    want = np.where(np.isinf(d), g.n, d).astype(np.int64)
+    want[g.s] = g.n
+    assert np.array_equal(lv, want)
+
+
 def test_spec_global_relabel_example(golden):
     for ex in golden["global_relabel"]:
         g = _g(ex["n"], ex["edges"], ex["s"], ex["t"])

@@ -149,3 +149,65 @@ def test_demerge_roundtrip():
     cf = b["cf0"] - x
     f = check.demerge_bcsr(g.n, g.row_off, g.col, g.cap, b["off"], b["col"], cf, b["cf0"], b["mate"])
     check.check_flow(g.n, g.row_off, g.col, g.cap, g.s, g.t, r.flow, r.in_S, f, strict=True)
+
+
+def test_demerge_rcsr_roundtrip():
+    # the RCSR analogue: a strict oracle flow written into the forward / backward residual
+    # capacities of the reference RCSR and de-merged again is valid (V1-V7 strict);
+    # antiparallel input edges stay distinct forward arcs in RCSR, so each arc carries only
+    # its own direction's flow: fcf = cap0 - f, bcf = f
+    g = synth.tiny_random(30, 200, 9, 5, self_loops=True)
+    r = oracle.maxflow_graph(g)
+    R = residual_ref.rcsr(g.n, g.row_off, g.col, g.cap)
+    owner = np.repeat(np.arange(g.n), np.diff(R["foff"]))
+    key = owner * g.n + R["fcol"]
+    src, dst, _ = g.edges()
+    keep = src != dst
+    fl = np.zeros(key.shape[0], np.int64)
+    np.add.at(fl, np.searchsorted(key, src[keep] * g.n + dst[keep]), r.edge_flow[keep])
+    fcf, bcf = R["fcf0"] - fl, fl
+    f = check.demerge_rcsr(g.n, g.row_off, g.col, g.cap, R["foff"], R["fcol"], fcf, R["fcf0"], bcf)
+    check.check_flow(g.n, g.row_off, g.col, g.cap, g.s, g.t, r.flow, r.in_S, f, strict=True)
+    # per parallel-edge group the de-merged flows sum to the arc flow
+    grp = np.searchsorted(key, src[keep] * g.n + dst[keep])
+    assert np.array_equal(np.bincount(grp, weights=f[keep], minlength=key.shape[0]).astype(np.int64), fl)
+    # corruptions are rejected: capacity not conserved, negative cf
+    bad = bcf.copy(); bad[int(np.argmax(bcf))] += 1
+    with pytest.raises(check.CheckError):
+        check.demerge_rcsr(g.n, g.row_off, g.col, g.cap, R["foff"], R["fcol"], fcf, R["fcf0"], bad)
+    bad = fcf.copy(); bad[int(np.argmin(fcf))] = -1
+    with pytest.raises(check.CheckError):
+        check.demerge_rcsr(g.n, g.row_off, g.col, g.cap, R["foff"], R["fcol"], bad, R["fcf0"], bcf - 0)
+
+
+def test_check_matching_rejects_mutations():
+    # matching validity: each pair an input edge, each l / r at most once, size
+    import synth as _s
+    from oracle import matching
+    nL, nR = 40, 30
+    l, r = _s.bipartite_edges(nL, nR, 120, 3)
+    n, src, dst, cap, s, t = matching.network(nL, nR, l, r)
+    g = _s.from_edges(n, src, dst, cap, s, t)
+    res = oracle.maxflow_graph(g)
+    # a matching from the oracle's strict flow: left l matched to r when the unit on (1+l, 1+nL+r) flows
+    gs, gd, _ = g.edges()
+    m = np.full(nL, -1, np.int64)
+    for i in np.nonzero(res.edge_flow > 0)[0]:
+        if 1 <= gs[i] <= nL and nL + 1 <= gd[i] <= nL + nR:
+            m[gs[i] - 1] = gd[i] - 1 - nL
+    assert matching.check_matching(nL, nR, l, r, m, res.flow)
+    with pytest.raises(AssertionError, match="expected"):
+        matching.check_matching(nL, nR, l, r, m, res.flow + 1)
+    li = int(np.nonzero(m >= 0)[0][0])
+    lj = int(np.nonzero(m >= 0)[0][1])
+    bad = m.copy(); bad[lj] = bad[li]                                   # right vertex used twice
+    with pytest.raises(AssertionError, match="twice"):
+        matching.check_matching(nL, nR, l, r, bad, res.flow)
+    edges = set(zip(l.tolist(), r.tolist()))
+    rr = next(x for x in range(nR) if (li, x) not in edges and x not in set(m.tolist()))
+    bad = m.copy(); bad[li] = rr                                        # not an input edge
+    with pytest.raises(AssertionError, match="not an input edge"):
+        matching.check_matching(nL, nR, l, r, bad, res.flow)
+    bad = m.copy(); bad[li] = nR                                        # out of range
+    with pytest.raises(AssertionError, match="out of range"):
+        matching.check_matching(nL, nR, l, r, bad, res.flow)
