@@ -22,16 +22,17 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gen.c")
+_SRCS = (_SRC, os.path.join(_HERE, "ingest.c"))
 _LIB = os.path.join(_HERE, "libsynth.so")
 _lock = threading.Lock()
 _lib = None
 
 
 def build(force: bool = False) -> str:
-    """Compile synth/gen.c into synth/libsynth.so (gcc -O3 -fopenmp)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    """Compile synth/gen.c + synth/ingest.c into synth/libsynth.so (gcc -O3 -fopenmp)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        cmd = ["gcc", "-O3", "-march=x86-64-v2", "-fopenmp", "-shared", "-fPIC", _SRC, "-o", tmp]
+        cmd = ["gcc", "-O3", "-march=x86-64-v2", "-fopenmp", "-shared", "-fPIC", *_SRCS, "-o", tmp]
         subprocess.run(cmd, check=True)
         os.replace(tmp, _LIB)
     return _LIB
@@ -71,6 +72,13 @@ def _L():
             lib.synth_genrmf.restype = i64
             lib.synth_draw.argtypes = [u64, u64, u64]
             lib.synth_draw.restype = u64
+            for f in (lib.ingest_dimacs, lib.ingest_konect):
+                f.argtypes = [ctypes.c_char_p, ctypes.POINTER(_IngestResult)]
+                f.restype = i32
+            lib.ingest_snap.argtypes = [ctypes.c_char_p, i32, ctypes.POINTER(_IngestResult)]
+            lib.ingest_snap.restype = i32
+            lib.ingest_free.argtypes = [ctypes.POINTER(_IngestResult)]
+            lib.ingest_free.restype = None
             lib.synth_set_threads.argtypes = [i32]
             lib.synth_set_threads.restype = None
             # (torchrun exports OMP_NUM_THREADS=1 to every rank: use this rank's share of the cores)
@@ -85,6 +93,14 @@ def _L():
                 lib.synth_set_threads(int(nt))
             _lib = lib
     return _lib
+
+
+class _IngestResult(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64),
+                ("src", ctypes.POINTER(ctypes.c_int32)), ("dst", ctypes.POINTER(ctypes.c_int32)),
+                ("cap", ctypes.POINTER(ctypes.c_int32)), ("s", ctypes.c_int64), ("t", ctypes.c_int64),
+                ("nL", ctypes.c_int64), ("nR", ctypes.c_int64), ("declared_m", ctypes.c_int64),
+                ("self_loops", ctypes.c_int64), ("duplicates", ctypes.c_int64), ("err_line", ctypes.c_int64)]
 
 
 def _p(a: np.ndarray):
@@ -321,3 +337,84 @@ def genrmf(a: int = 128, b: int = 128, c1: int = 1, c2: int = 10000, seed: int =
     assert k == m
     n = a * a * b
     return from_edges(n, src, dst, cap, 0, n - 1, name=f"genrmf-{a}x{b}", config="S1")
+
+
+# --------------------------------------------------------------------------- dataset files (NEXT #4)
+class IngestError(ValueError):
+    """A dataset file that does not parse (code, 1-based line)."""
+
+    MESSAGES = {-1: "cannot open or read the file", -2: "no 'p max' problem line",
+                -3: "no source or no sink designated", -4: "malformed line",
+                -5: "vertex id out of range", -6: "capacity out of range", -7: "out of memory"}
+
+    def __init__(self, path, code, line):
+        self.code, self.line = int(code), int(line)
+        super().__init__(f"{path}: {self.MESSAGES.get(self.code, 'error')}"
+                         + (f" at line {self.line}" if self.line else "") + f" (code {self.code})")
+
+
+def _ingest(fn, path, *args):
+    r = _IngestResult()
+    rc = fn(os.fsencode(path), *args, ctypes.byref(r))
+    if rc != 0:
+        raise IngestError(path, rc, r.err_line)
+    try:
+        m = int(r.m)
+
+        def take(ptr):
+            if m == 0 or not ptr:
+                return np.zeros(0, np.int32)
+            return np.ctypeslib.as_array(ptr, shape=(m,)).copy()
+        out = dict(n=int(r.n), src=take(r.src), dst=take(r.dst), cap=take(r.cap) if r.cap else None,
+                   s=int(r.s), t=int(r.t), nL=int(r.nL), nR=int(r.nR), declared_m=int(r.declared_m),
+                   self_loops=int(r.self_loops), duplicates=int(r.duplicates))
+    finally:
+        _L().ingest_free(ctypes.byref(r))
+    return out
+
+
+def read_dimacs(path: str) -> Graph:
+    """DIMACS max-flow file (`p max N M`, `n ID s|t`, `a U V CAP`, 1-based) -> Graph with its
+    designated s and t (the Washington / Genrmf networks of Table 1).
+    meta['declared_m'] is the problem line's arc count (a mismatch is reported, not fatal)."""
+    d = _ingest(_L().ingest_dimacs, path)
+    return from_edges(d["n"], d["src"], d["dst"], d["cap"], d["s"], d["t"], name=os.path.basename(path),
+                      config="dimacs", declared_m=d["declared_m"], arc_count_mismatch=d["declared_m"] != len(d["src"]))
+
+
+def write_dimacs(g: Graph, path: str, comment: str = "") -> None:
+    """Serialise a Graph as a DIMACS max-flow file (round-trip partner of read_dimacs)."""
+    src, dst, cap = g.edges()
+    with open(path, "w") as f:
+        if comment:
+            f.write(f"c {comment}\n")
+        f.write(f"p max {g.n} {g.m}\nn {g.s + 1} s\nn {g.t + 1} t\n")
+        body = np.stack([src.astype(np.int64) + 1, dst.astype(np.int64) + 1, cap.astype(np.int64)], axis=1)
+        np.savetxt(f, body, fmt="a %d %d %d")
+
+
+def read_snap(path: str, cap: int = 1):
+    """SNAP edge list -> (n, src, dst, cap): ids remapped densely in order of first appearance,
+    self-loops dropped, duplicate lines merged with their capacities summed (S:338-350);
+    capacity `cap` per line ("The edge capacity of graphs in SNAP is set to 1", Table 1)."""
+    d = _ingest(_L().ingest_snap, path, int(cap))
+    return d["n"], d["src"], d["dst"], d["cap"]
+
+
+def snap_instance(path: str, npairs: int = 20, nstarts: int = 256, seed: int = 1, cap: int = 1) -> Graph:
+    """A SNAP network as the paper's multi-source multi-sink instance: `npairs`
+    BFS-selected source/sink pairs (the same rule as C3, `select_pairs`) behind a super-source
+    and a super-sink with incident-sum capacities."""
+    n, src, dst, c = read_snap(path, cap)
+    ro, col, _ = csr_from_edges(n, src, dst, c)
+    so, si = select_pairs(n, ro, col, npairs, nstarts, seed)
+    N, src2, dst2, cap2, S, T = add_super_terminals(n, src, dst, c, so, si)
+    return from_edges(N, src2, dst2, cap2, S, T, name=os.path.basename(path), config="snap",
+                      sources=so.tolist(), sinks=si.tolist())
+
+
+def read_konect(path: str):
+    """KONECT bipartite edge list -> (nL, nR, l, r) with 0-based ids per side, weights ignored,
+    duplicate pairs collapsed; side sizes = max(header `% E L R`, largest id)."""
+    d = _ingest(_L().ingest_konect, path)
+    return d["nL"], d["nR"], d["src"], d["dst"]

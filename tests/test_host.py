@@ -177,3 +177,15 @@ def test_bench_rejects_world_mismatch():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--dry-run"],
                        capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr
+
+
+def test_package_exports_every_binding_entry_point():
+    """bench.py / tools / tests call the binding through the package (`W.name`): every public
+    function of wbpr.py is re-exported (a missing export silently dropped the latency floor)."""
+    import inspect
+    import paper_2404_00270_b200 as W
+    from paper_2404_00270_b200 import wbpr
+    public = [n for n, f in inspect.getmembers(wbpr, inspect.isfunction)
+              if not n.startswith("_") and f.__module__ == wbpr.__name__]
+    missing = [n for n in public if not hasattr(W, n)]
+    assert not missing, missing
