@@ -327,9 +327,15 @@ def latency_floor(sts, ns_phase):
     ph = [sum(s["phase_count"][:9]) for s in sts]
     small = [s["phase_count"][9] for s in sts]
     fl = [p * ns_phase / 1e6 for p in ph]
+    names = ["none", "round", "gr_reset", "bfs_top_down", "compact", "preflow", "gap_lift", "async_bfs",
+             "bfs_bottom_up", "small_mode"]
+    by_kind = {nm: {"ms": round(float(np.median([s["phase_ns"][i] for s in sts]) / 1e6), 3),
+                    "phases": int(np.median([s["phase_count"][i] for s in sts]))}
+               for i, nm in enumerate(names) if any(s["phase_count"][i] for s in sts)}
     return {"grid_phases_per_solve": int(np.median(ph)), "small_mode_phases_per_solve": int(np.median(small)),
             "ns_per_empty_phase": round(ns_phase, 1), "floor_ms": round(float(np.median(fl)), 3),
-            "floor_share_of_solve": round(float(np.median([f / s["solve_ms"] for f, s in zip(fl, sts)])), 4)}
+            "floor_share_of_solve": round(float(np.median([f / s["solve_ms"] for f, s in zip(fl, sts)])), 4),
+            "phase_time_by_kind": by_kind}
 
 
 # ---------------------------------------------------------------------------- device helpers
@@ -348,7 +354,7 @@ def parse_opts(args, workload):
     return opt
 
 
-def graph_line(name, g, dev, layout, reps=5, warmup=2, opt=None):
+def graph_line(name, g, dev, layout, reps=5, warmup=2, opt=None, ns_phase=None):
     """Per-graph sub-line: `reps` device-resident solves (each preceded by an L2 flush),
     median / min / max of the library's own CUDA-event windows, roofline from each solve's
     own counters; returns (line, gpu result for the parity gate)."""
@@ -375,13 +381,17 @@ def graph_line(name, g, dev, layout, reps=5, warmup=2, opt=None):
             "counters_median_run": {k: med[k] for k in ("rounds", "global_relabels", "bfs_levels", "pushes", "relabels",
                                                         "arcs_scanned", "bfs_arcs_scanned", "bfs_arcs_bottom_up")},
             "roofline": dict(bound="hbm", kernel="k_solve", peak=hbm, unit="GB/s", **roofline_of(sts, hbm)),
+            "latency_floor": latency_floor(sts, ns_phase),
             "flow": int(F), "cut_capacity": int(med["cut_capacity"])}
+    tr, tr_cap = traffic_of(name, layout)
+    line["roofline"]["traffic"] = tr
+    line["roofline"]["traffic_same_capture"] = tr_cap
     del ws, ro, col, cap
     torch.cuda.empty_cache()
     return line, (int(F), int(med["cut_capacity"]), words)
 
 
-def bipartite_line(wl, dev, layout, reps=5, warmup=2):
+def bipartite_line(wl, dev, layout, reps=5, warmup=2, ns_phase=None):
     import torch
     import paper_2404_00270_b200 as W
     nL, nR = wl["nL"], wl["nR"]
@@ -405,7 +415,11 @@ def bipartite_line(wl, dev, layout, reps=5, warmup=2):
             "counters_median_run": {k: med[k] for k in ("rounds", "global_relabels", "bfs_levels", "pushes", "relabels",
                                                         "arcs_scanned", "bfs_arcs_scanned", "bfs_arcs_bottom_up")},
             "roofline": dict(bound="hbm", kernel="k_solve", peak=hbm, unit="GB/s", **roofline_of(sts, hbm)),
+            "latency_floor": latency_floor(sts, ns_phase),
             "matching_size": int(size)}
+    tr, tr_cap = traffic_of("c4", layout)
+    line["roofline"]["traffic"] = tr
+    line["roofline"]["traffic_same_capture"] = tr_cap
     m_host = match.cpu().numpy().copy()
     del ws, l_d, r_d
     torch.cuda.empty_cache()
@@ -559,21 +573,21 @@ def run_wbpr(args, rank, world, local_rank):
     e2e_value = total_units * e2e_steps / (e2e_ms / 1e3) if args.e2e_streams > 0 else None
     del ws
     torch.cuda.empty_cache()
-    # ---- per-graph sub-lines (device work; N = 1 default run)
-    per_graph, gpu_extra = {}, {}
-    for name, g in extra.items():
-        if isinstance(g, dict):
-            per_graph[name], gpu_extra[name] = bipartite_line(g, dev, args.layout)
-        else:
-            per_graph[name], gpu_extra[name] = graph_line(name, g, dev, args.layout,
-                                                          reps=3 if name == "c2r" else 5,
-                                                          warmup=1 if name == "c2r" else 2)
     # ---- barrier-latency floor (an empty grid phase of the persistent kernel)
     try:
         ns_phase = W.barrier_cost(0, 4000, dev)
     except Exception as ex:   # measurement helper only
         log("barrier probe failed:", ex)
         ns_phase = None
+    # ---- per-graph sub-lines (device work; N = 1 default run)
+    per_graph, gpu_extra = {}, {}
+    for name, g in extra.items():
+        if isinstance(g, dict):
+            per_graph[name], gpu_extra[name] = bipartite_line(g, dev, args.layout, ns_phase=ns_phase)
+        else:
+            per_graph[name], gpu_extra[name] = graph_line(name, g, dev, args.layout,
+                                                          reps=3 if name == "c2r" else 5,
+                                                          warmup=1 if name == "c2r" else 2, ns_phase=ns_phase)
     # ---- parity gate + cpu_baseline leg (after all device timing)
     parity, cpu = None, None
     if pool is not None:
@@ -735,7 +749,12 @@ def run_bipartite_main(args, rank, world, dev, wl, gen_s, pool):
         size, match, st = W.bipartite_match(nL, nR, l_d, r_d, workspace=ws, **opt)
         if host:
             match_h.copy_(match, non_blocking=True)
+        elif args.dump_steps:
+            dumped.append(dict(solve_bytes=solve_bytes(st), **{k_: v_ for k_, v_ in st.items()
+                                                               if not isinstance(v_, list)}))
         return size, match, st
+
+    dumped = []
 
     for _ in range(args.warmup):
         step()
@@ -756,14 +775,17 @@ def run_bipartite_main(args, rank, world, dev, wl, gen_s, pool):
     ms = evs[0].elapsed_time(evs[-1])
     step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     m_gpu = match.cpu().numpy().copy()
-    e2e_steps = max(1, min(args.steps, 5))
+    if args.dump_steps:
+        with open(f"{args.dump_steps}.rank{rank}", "w") as f:
+            json.dump(dumped, f)
+    e2e_steps = max(1, min(args.steps, 5)) if args.e2e_streams > 0 else 0   # 0: profiler runs (no e2e leg)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
         step(host=True)
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    e2e_ms = e0.elapsed_time(e1)
+    e2e_ms = e0.elapsed_time(e1) if e2e_steps else float("nan")
     times = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(times, op=dist.ReduceOp.MAX)
     ms, e2e_ms = float(times[0]), float(times[1])
@@ -810,7 +832,7 @@ def run_bipartite_main(args, rank, world, dev, wl, gen_s, pool):
         "roofline": {"bound": "hbm", "kernel": "k_solve (persistent push-relabel + device GR, 1 launch/step)",
                      "achieved": roof["achieved"], "peak": hbm, "peak_source": peak_src, "unit": "GB/s",
                      "frac": roof["frac"], "traffic": traffic, "traffic_same_capture": traffic_cap, "detail": roof},
-        "e2e": {"value": round(world * e2e_steps / (e2e_ms / 1e3), 3), "unit": "matchings/s",
+        "e2e": {"value": round(world * e2e_steps / (e2e_ms / 1e3), 3) if e2e_steps else None, "unit": "matchings/s",
                 "h2d_bytes_per_step": int(wl["l"].nbytes + wl["r"].nbytes), "d2h_bytes_per_step": 4 * nL,
                 "steps": e2e_steps},
         "gpu_launches": int(sum(x["kernel_launches"] for x in sts)),

@@ -178,6 +178,10 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
       ++r;
     }
     a.seg[x] = make_int2(slot0, slot0 + r);
+    // unused slots after the segment (merged duplicates, self-loops) are zeroed: the solver's
+    // 16-B vector loads may cover them (values masked, but never uninitialised)
+    if (PASS == 1)
+      for (int g = slot0 + r; g < slot0 + lo + li; ++g) a.arc[g] = make_int2(0, 0);
     msum += r;
   }
   if (PASS == 1) {
@@ -281,6 +285,7 @@ __global__ void __launch_bounds__(256) k_merge_warp(MergeArgs a) {
     const int base = ob + ib;   // gapped layout (see k_merge_thread)
     int h = warp_merge_range<1>(a, ob, lo, ib, li, 0, 0, 0, lo + li, kInf, base);
     if (lane == 0) { a.seg[x] = make_int2(base, base + h); atomicAdd(&a.ctrl->M, h); }
+    for (int g = base + h + lane; g < base + lo + li; g += 32) a.arc[g] = make_int2(0, 0);   // unused tail
   }
 }
 
@@ -330,10 +335,13 @@ __global__ void __launch_bounds__(256) k_merge_chunk(MergeArgs a) {
       before = warp_sum(before);
       const int base = ob + ib;   // gapped layout (see k_merge_thread)
       warp_merge_range<1>(a, ob, lo, ib, li, i0, j0, k0, k1, prev, base + before);
-      if (c == 0 && lane == 0) {
+      if (c == 0) {
         const int d = __ldg(a.mdeg + x);
-        a.seg[x] = make_int2(base, base + d);
-        atomicAdd(&a.ctrl->M, d);
+        if (lane == 0) {
+          a.seg[x] = make_int2(base, base + d);
+          atomicAdd(&a.ctrl->M, d);
+        }
+        for (int g = base + d + lane; g < base + total; g += 32) a.arc[g] = make_int2(0, 0);   // unused tail
       }
     }
   }

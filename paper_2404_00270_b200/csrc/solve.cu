@@ -199,6 +199,14 @@ constexpr int kBuThread = WBPR_BUT; // bottom-up BFS: vertices up to this many s
 #ifndef WBPR_BUB
 #define WBPR_BUB 8
 #endif
+#ifndef WBPR_BU_ALPHA
+#define WBPR_BU_ALPHA 7   // measured (3 x 20-step A/B, tools/sweep_bu.sh): C5 solve 11.4 -> 9.9 ms, C1 0.74 -> 0.58 ms,
+#endif                    // C3 / C3h equal, C4 +0.5 ms (14 was the previous default; 4 and 1 no better)
+#ifndef WBPR_BU_BETA
+#define WBPR_BU_BETA 24
+#endif
+constexpr int kBuAlpha = WBPR_BU_ALPHA;   // go bottom-up when frontier slots * alpha > slots not yet labelled (Beamer)
+constexpr int kBuBeta = WBPR_BU_BETA;     // back to top-down when the frontier holds < n / beta vertices
 constexpr int kBuB = WBPR_BUB;    // bottom-up BFS: slots loaded per batch (independent loads)
 // neighbour-label gathers: L2-only (default) or L1-allocating
 #ifndef WBPR_H_L1
@@ -419,8 +427,8 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
           unsigned long long Mtot = (unsigned long long)Mslots;
           if (G.prev_reached && G.prev_reached < Mtot) Mtot = G.prev_reached;
           const unsigned long long rest = Mtot > G.bfs_seen_edges ? Mtot - G.bfs_seen_edges : 0;
-          if (!G.bfs_bottom_up) G.bfs_bottom_up = P.bfs_mode != 0 && fe * 14ull > rest;
-          else G.bfs_bottom_up = (long long)qn * 24 >= (long long)(VHI - VLO);
+          if (!G.bfs_bottom_up) G.bfs_bottom_up = P.bfs_mode != 0 && fe * (unsigned long long)kBuAlpha > rest;
+          else G.bfs_bottom_up = (long long)qn * kBuBeta >= (long long)(VHI - VLO);
           if (P.bfs_mode == 2) G.bfs_bottom_up = 1;
           if (G.bfs_bottom_up) flags |= 2;
           // bfs_mode 3: a deep GR continues as the asynchronous label-correcting BFS
@@ -785,7 +793,9 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
         int code = 0, nn = 0;
         __syncthreads();
         while (true) {
-          if (threadIdx.x == 0) { S.s_n = 0; S.s_maxdeg = 0; S.s_huge = 0; S.s_work = 0; S.s_exit = 0; }
+          // (s_exit is not reset here: thread 0 writes it every phase between the two barriers
+          // below, and a reset here would race with the other threads' read of the previous one)
+          if (threadIdx.x == 0) { S.s_n = 0; S.s_maxdeg = 0; S.s_huge = 0; S.s_work = 0; }
           sdst = (state == S_BFS) ? (fb ^ 1) : (cur ^ 1);
           __syncthreads();
           if (state == S_BFS) {
