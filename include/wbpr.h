@@ -137,6 +137,16 @@ typedef struct wbpr_options {
                             view exposes the compacted AVQ (Alg. 2 l.1-4).  The
                             flow value is not final and the certificate is not checked.
                             0 (default): off                                                 */
+  int32_t tiny_mode;     /* 0 (default): a single BCSR instance with n <= 2048 vertices and
+                            2m <= 16384 half-arcs (C1-sized) runs the whole path - A1
+                            construction, preflow, rounds, global relabels, extraction - in ONE
+                            launch of ONE CTA with the residual graph in shared memory
+                            (tiny.cu); launch- and barrier-latency, not work, bounds such
+                            instances.  Same readings and results; options that need the
+                            persistent kernel (RCSR, thread-centric, phase 2, traces, online
+                            gap, push_mode 0, debug_stop, grid_blocks > 0, bfs_mode != 1,
+                            l2_persist) use it instead.
+                            1: always the multi-kernel path                                  */
 } wbpr_options;
 
 typedef struct wbpr_stats {
@@ -169,6 +179,7 @@ typedef struct wbpr_stats {
   int64_t bfs_arcs_bottom_up; /* the part of bfs_arcs_scanned read by bottom-up levels (a
                                  slot's own {col, cf} + h[col]: 12 B); the rest are top-down
                                  in-arcs (col, mate, cf[mate], h: 16 B) - DESIGN.md §5      */
+  int64_t tiny_path;         /* 1: this call ran the one-CTA fused path (tiny_mode)        */
 } wbpr_stats;
 
 /* Fill *opt with the defaults above. */

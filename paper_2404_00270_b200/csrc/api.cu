@@ -271,6 +271,111 @@ struct Events {
   }
 };
 
+// The one-CTA fused path (tiny.cu) for a tiny single BCSR instance: one launch, the result
+// record back through the pinned scratch, one synchronisation.
+wbpr_status solve_tiny(const wbpr_csr* g, int64_t s_v, int64_t t_v, const wbpr_options& opt, const Ws& W,
+                       uint32_t* bitmap, int64_t* flow_out, int64_t* cut_out, wbpr_stats* stats, cudaStream_t st) {
+  const Layout& L = W.L;
+  void* ws = W.base;
+  const int64_t n = g->n, m = g->m;
+  const long long launches0 = launch_count();
+  Events E;
+  CK(E.create());
+  SyncOnExit guard{st};
+  guard.armed = true;
+  CK(cudaEventRecord(E.ev[0], st));
+  const int64_t* ro = g->row_offsets;
+  const int32_t* col = g->col;
+  const int32_t* cap = g->cap;
+  if (g->on_host) {
+    CK(cudaMemcpyAsync(at<int64_t>(ws, L.in_row), ro, 8 * (n + 1), cudaMemcpyHostToDevice, st));
+    if (m > 0) {
+      CK(cudaMemcpyAsync(at<int32_t>(ws, L.in_col), col, 4 * m, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(at<int32_t>(ws, L.in_cap), cap, 4 * m, cudaMemcpyHostToDevice, st));
+    }
+    ro = at<int64_t>(ws, L.in_row);
+    col = at<int32_t>(ws, L.in_col);
+    cap = at<int32_t>(ws, L.in_cap);
+  }
+  uint32_t* dbm = bitmap;
+  if (bitmap && g->on_host) dbm = reinterpret_cast<uint32_t*>(at<int>(ws, L.q0));
+  TinyArgs a{};
+  a.ro = ro; a.col = col; a.cap = cap;
+  a.n = (int)n; a.m = (int)m; a.s = (int)s_v; a.t = (int)t_v;
+  a.seg = at<int2>(ws, L.seg); a.arc = at<int2>(ws, L.regC); a.mate = at<int>(ws, L.regB);
+  a.cap0 = at<int>(ws, L.regB + L.bcap0);
+  a.h = at<int>(ws, L.h); a.e = at<long long>(ws, L.e);
+  a.bitmap = dbm;
+  a.flow = at<long long>(ws, L.inst_flow); a.cut = at<long long>(ws, L.inst_cut);
+  a.ctrl = W.ctrl;
+  a.gr_beta = opt.gr_beta;
+  a.max_rounds = opt.max_rounds > 0 ? opt.max_rounds : 10 * n + 1000;
+  a.deadline_ns_rel = (unsigned long long)opt.timeout_ms * 1000000ull;
+  CK(launch_tiny(a, st));
+  CK(cudaEventRecord(E.ev[1], st));
+  char* pin = g_pin.get(sizeof(Ctrl) + 16 + 64);
+  Ctrl c;
+  long long F = 0, Cc = 0;
+  if (pin) {
+    CK(cudaMemcpyAsync(pin, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pin + sizeof(Ctrl), a.flow, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pin + sizeof(Ctrl) + 8, a.cut, 8, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(&c, W.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&F, a.flow, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&Cc, a.cut, 8, cudaMemcpyDeviceToHost, st));
+  }
+  if (bitmap && g->on_host) CK(cudaMemcpyAsync(bitmap, dbm, 4 * ((n + 31) / 32), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(E.ev[2], st));
+  CK(cudaStreamSynchronize(st));
+  guard.armed = false;
+  if (pin) { memcpy(&c, pin, sizeof(Ctrl)); memcpy(&F, pin + sizeof(Ctrl), 8); memcpy(&Cc, pin + sizeof(Ctrl) + 8, 8); }
+  const int64_t bad_edge = c.bad_edge == LLONG_MAX ? -1 : c.bad_edge;
+  if (stats) {
+    memset(stats, 0, sizeof(*stats));
+    stats->n = n; stats->m = m; stats->bad_edge_index = bad_edge;
+    stats->tiny_path = 1;
+  }
+  if (c.bad_rows) return fail(WBPR_EINVAL, "row_offsets are not a valid CSR offset array");
+  if (bad_edge >= 0)
+    return fail(WBPR_EINVAL, "edge " + std::to_string(bad_edge) +
+                                 " has a column outside its instance's range or a negative capacity");
+  register_view(W, WBPR_LAYOUT_BCSR, c.M, c.M);
+  if (c.overflow) return fail(WBPR_EOVERFLOW, "merged capacity exceeds INT32_MAX");
+  if (flow_out) flow_out[0] = F;
+  if (cut_out) cut_out[0] = Cc;
+  if (stats) {
+    stats->flow_value = F;
+    stats->cut_capacity = Cc;
+    stats->M = c.M;
+    stats->rounds = c.stats[ST_ROUNDS];
+    stats->global_relabels = c.stats[ST_GRS];
+    stats->bfs_levels = c.stats[ST_BFS_LEVELS];
+    stats->pushes = c.stats[ST_PUSHES];
+    stats->relabels = c.stats[ST_RELABELS];
+    stats->arcs_scanned = c.stats[ST_ARCS];
+    stats->bfs_arcs_scanned = c.stats[ST_BFS_ARCS];
+    stats->self_loops_ignored = c.selfloops;
+    stats->excess_total = c.excess_total;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, E.ev[0], E.ev[1]);
+    stats->total_ms = ms;
+    stats->build_ms = (float)((double)c.phase_ns[PK_NONE] / 1e6);
+    if (stats->build_ms > ms) stats->build_ms = ms;
+    stats->solve_ms = ms - stats->build_ms;
+    cudaEventElapsedTime(&ms, E.ev[1], E.ev[2]); stats->extract_ms = ms;
+    stats->grid_blocks = 1;
+    stats->block_threads = 1024;
+    for (int i = 0; i < kPhBuckets; ++i) { stats->phase_ns[i] = c.phase_ns[i]; stats->phase_count[i] = c.phase_cnt[i]; }
+    stats->kernel_launches = launch_count() - launches0;
+  }
+  if (c.status == DS_NOTCONVERGED) return fail(WBPR_ENOTCONVERGED, "round cap exceeded");
+  if (c.abort || c.status == DS_TIMEOUT) return fail(WBPR_ENOTCONVERGED, "device watchdog timeout");
+  if (F != Cc) return fail(WBPR_EINTERNAL, "certificate failed: cut capacity != flow value");
+  if (F != c.excess_total) return fail(WBPR_EINTERNAL, "Excess_total bookkeeping disagrees with e(t)");
+  return WBPR_OK;
+}
+
 // Shared driver of single and batch solves.
 wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const int64_t* s_h, const int64_t* t_h,
                        const wbpr_options* opt_in, void* ws, size_t ws_bytes, uint32_t* bitmap, int64_t* flow_out,
@@ -305,6 +410,10 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   if (opt.debug_stop < 0) return fail(WBPR_EINVAL, "debug_stop must be >= 0");
   if (opt.debug_stop > 0 && (k != 1 || opt.phase2 || opt.schedule != 0))
     return fail(WBPR_EINVAL, "debug_stop needs a single-instance vertex-centric phase-1 solve");
+  if (opt.tiny_mode == 0 && k == 1 && !build_only && opt.layout == WBPR_LAYOUT_BCSR && opt.schedule == 0 &&
+      !opt.phase2 && opt.trace_rounds <= 0 && opt.gap_mode == 0 && opt.push_mode == 1 && opt.debug_stop == 0 &&
+      opt.grid_blocks == 0 && opt.bfs_mode == 1 && !opt.l2_persist && tiny_fits(n, m))
+    return solve_tiny(g, s_h[0], t_h[0], opt, W, bitmap, flow_out, cut_out, stats, st);
   const long long launches0 = launch_count();
   Events E;
   CK(E.create());

@@ -221,6 +221,22 @@ inline Layout make_layout(int64_t n, int64_t m, int64_t k, int32_t layout, int32
   return L;
 }
 
+// One-CTA fused path for tiny single instances (tiny.cu): limits and launch arguments.
+constexpr int kTinyN = 2048;     // vertices
+constexpr int kTinyS = 16384;    // half-arcs (2m)
+struct TinyArgs {
+  const int64_t* ro; const int32_t* col; const int32_t* cap;   // input CSR (device)
+  int n, m, s, t;
+  int2* seg; int2* arc; int* mate; int* cap0;                  // BCSR in the workspace (residual view)
+  int* h; long long* e;
+  uint32_t* bitmap;                                            // nullptr: no bitmap
+  long long* flow; long long* cut;                             // per-instance results [1]
+  Ctrl* ctrl;
+  float gr_beta;
+  long long max_rounds;
+  unsigned long long deadline_ns_rel;
+};
+
 // Launch parameters of the persistent solve kernel.
 struct SolveParams {
   Ctrl* ctrl;

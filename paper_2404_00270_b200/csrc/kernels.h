@@ -94,4 +94,8 @@ void bip_build(int64_t nL, int64_t nR, int64_t E, const int32_t* l, const int32_
 void bip_extract(const SolveParams& p, int64_t nL, int64_t nR, int32_t* match_of_left, int num_sms,
                  cudaStream_t st);
 
+// tiny.cu: the whole path in one launch of one CTA (tiny single instances)
+bool tiny_fits(int64_t n, int64_t m);
+cudaError_t launch_tiny(const TinyArgs& a, cudaStream_t st);
+
 }  // namespace wbpr

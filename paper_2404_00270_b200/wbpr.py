@@ -46,7 +46,7 @@ class Options(ctypes.Structure):
                 ("push_mode", ctypes.c_int32), ("gr_gamma", ctypes.c_float), ("l2_persist", ctypes.c_int32),
                 ("bfs_mode", ctypes.c_int32), ("small_mode", ctypes.c_int32), ("schedule", ctypes.c_int32),
                 ("phase2", ctypes.c_int32), ("trace_rounds", ctypes.c_int32), ("batch_groups", ctypes.c_int32),
-                ("debug_stop", ctypes.c_int32)]
+                ("debug_stop", ctypes.c_int32), ("tiny_mode", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -58,7 +58,7 @@ class Stats(ctypes.Structure):
         ("total_ms", ctypes.c_float), ("grid_blocks", ctypes.c_int32), ("block_threads", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int64), ("t_barrier_ns", ctypes.c_int64), ("t_flush_ns", ctypes.c_int64),
         ("t_round_ns", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 10), ("phase_count", ctypes.c_int64 * 10),
-        ("bfs_arcs_bottom_up", ctypes.c_int64)]
+        ("bfs_arcs_bottom_up", ctypes.c_int64), ("tiny_path", ctypes.c_int64)]
 
     def as_dict(self):
         d = {}
@@ -128,7 +128,8 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
             l2_persist: Optional[int] = None, bfs_mode: Optional[int] = None,
             small_mode: Optional[int] = None, schedule: Optional[str] = None,
             phase2: Optional[int] = None, trace_rounds: Optional[int] = None,
-            batch_groups: Optional[int] = None, debug_stop: Optional[int] = None) -> Options:
+            batch_groups: Optional[int] = None, debug_stop: Optional[int] = None,
+            tiny_mode: Optional[int] = None) -> Options:
     o = Options()
     _check(load().wbpr_default_options(ctypes.byref(o)))
     o.layout = _LAYOUTS[layout]
@@ -159,6 +160,8 @@ def options(layout="bcsr", gr_beta: float = 0.0, gap_mode: int = 0, max_rounds: 
         o.batch_groups = batch_groups
     if debug_stop is not None:
         o.debug_stop = debug_stop
+    if tiny_mode is not None:
+        o.tiny_mode = tiny_mode
     return o
 
 

@@ -81,7 +81,15 @@ def _worker(rank, world, port, q):
     flows = [oracle.maxflow_graph(g, phase2=False).flow for g in parts]
     rec = torch.from_numpy(make_records(list(range(lo, hi)), flows, flows))
     allrec = gather_records(rec, total, world)
+    # the bench's timed-loop form: static per-rank counts (uneven: 7 over 2 ranks), one
+    # all_gather_into_tensor, ordered after the fact
+    from paper_2404_00270_b200.batch import gather_records_async, order_records
+    counts = [partition(7, world, r)[1] - partition(7, world, r)[0] for r in range(world)]
+    lo7, hi7 = partition(7, world, rank)
+    rec7 = torch.from_numpy(make_records(list(range(lo7, hi7)), [10 * i for i in range(lo7, hi7)], [0] * (hi7 - lo7)))
+    all7 = order_records(gather_records_async(rec7, counts, world), 7)
     if rank == 0:
+        assert all7[:, 0].tolist() == list(range(7)) and all7[:, 2].tolist() == [10 * i for i in range(7)]
         q.put(allrec.numpy().tolist())
     dist.destroy_process_group()
 
