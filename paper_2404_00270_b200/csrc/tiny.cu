@@ -388,7 +388,9 @@ __global__ void __launch_bounds__(kTinyThreads, 1) k_tiny(TinyArgs A) {
         for (int p = b; p < e_; ++p) {
           const int u = S.r.col[p];
           // residual in-arc u -> x: c_f(u, x) = cf[mate[p]]
-          if (S.h[u] == N && S.r.cf[S.r.mate[p]] > 0) S.h[u] = level + 1;   // (any writer wins)
+          // (labels are written with atomics: concurrent plain reads of them are the
+          // algorithm's benign races, never a torn or lost value)
+          if (S.h[u] == N && S.r.cf[S.r.mate[p]] > 0) atomicCAS(&S.h[u], N, level + 1);
         }
       }
       for (int j = w; j < qa; j += kTinyWarps) {
@@ -398,10 +400,11 @@ __global__ void __launch_bounds__(kTinyThreads, 1) k_tiny(TinyArgs A) {
         for (int p = b + lane; p < e_; p += 32) {
           const int u = S.r.col[p];
           ++arcs;
-          if (S.h[u] == N && S.r.cf[S.r.mate[p]] > 0) S.h[u] = level + 1;
+          if (S.h[u] == N && S.r.cf[S.r.mate[p]] > 0) atomicCAS(&S.h[u], N, level + 1);
         }
       }
       tot_bfs += arcs;   // (per-thread; summed once at the end)
+      __syncwarp();
       __syncthreads();
       // next frontier = the vertices labelled level + 1 (a compaction over n with one
       // shared atomic per warp, instead of one contended append per discovered vertex)
@@ -452,8 +455,10 @@ __global__ void __launch_bounds__(kTinyThreads, 1) k_tiny(TinyArgs A) {
         base = __shfl_sync(FULL, base, 0);
         if (act) S.s.q[0][base + __popc(bm & ((1u << lane) - 1u))] = (uint16_t)v;
       }
+      __syncwarp();
       __syncthreads();
       const int qa = S.qn[0];
+      __syncthreads();      // (everyone has read qa before the GR below rewrites S.qn)
       if (qa == 0) break;   // queue empty: exact GR decides termination
       long long pushes = 0, relabels = 0, arcs = 0;
       // active vertices with <= kTinyThr slots: one THREAD each (the same push / relabel
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(kTinyThreads, 1) k_tiny(TinyArgs A) {
           }
           if (sent) atomicAdd((unsigned long long*)&S.s.e[u], (unsigned long long)(-sent));
         } else {
-          S.h[u] = best == ~0ull ? N : min(N, (int)(best >> 32) + 1);
+          atomicExch(&S.h[u], best == ~0ull ? N : min(N, (int)(best >> 32) + 1));
           ++relabels;
           atomicAdd(&S.work, (unsigned)(e_ - b));
         }
@@ -542,12 +547,13 @@ __global__ void __launch_bounds__(kTinyThreads, 1) k_tiny(TinyArgs A) {
           if (lane == 0 && sent) atomicAdd((unsigned long long*)&S.s.e[u], (unsigned long long)(-sent));
         } else if (lane == 0) {
           // relabel to the lowest residual neighbour + 1 (no residual arc: unreachable, n)
-          S.h[u] = best == ~0ull ? N : min(N, (int)(best >> 32) + 1);
+          atomicExch(&S.h[u], best == ~0ull ? N : min(N, (int)(best >> 32) + 1));
           ++relabels;
           atomicAdd(&S.work, (unsigned)(e_ - b));
         }
       }
       tot_push += pushes; tot_rel += relabels; tot_arcs += arcs;   // (per-thread; summed at the end)
+      __syncwarp();
       ++rounds;
       if (tid == 0) {
         const unsigned long long x = globaltimer();
@@ -556,9 +562,9 @@ __global__ void __launch_bounds__(kTinyThreads, 1) k_tiny(TinyArgs A) {
       }
       __syncthreads();
       status = S.flag;
-      if (status != DS_OK) break;
       gr_due = S.work >= gr_threshold;
       __syncthreads();   // (S.flag / S.work are rewritten next round)
+      if (status != DS_OK) break;
     }
     if (status != DS_OK) break;
   }

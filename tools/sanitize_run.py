@@ -36,7 +36,8 @@ def main():
     c1 = synth.random_graph(1024, 8192, 1)
     if "c1" in which:
         for layout in ("bcsr", "rcsr"):
-            ok &= run(c1, layout=layout)
+            ok &= run(c1, layout=layout)          # (BCSR: the one-CTA tiny path)
+        ok &= run(c1, tiny_mode=1)                # the multi-kernel path on the same instance
         ok &= run(c1, schedule="tc")
     if "grid" in which:
         ok &= run(synth.grid(32, 32, True, 3))
