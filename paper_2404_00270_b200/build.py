@@ -55,14 +55,31 @@ def build(force: bool = False, verbose: bool = False, defines=(), variant: str =
     if not force and os.path.exists(out) and os.path.exists(stamp) and open(stamp).read() == dg:
         return out
 
+    hdr = hashlib.sha256()
+    for p in _headers():
+        with open(p, "rb") as f:
+            hdr.update(p.encode() + f.read())
+    hdr.update(" ".join(ARCH + FLAGS + list(defines)).encode())
+
     def comp(src):
         obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
+        # per-object digest (source + every header + flags): only changed sources recompile
+        h = hdr.copy()
+        with open(src, "rb") as f:
+            h.update(f.read())
+        odg = h.hexdigest()
+        ostamp = obj + ".digest"
+        if (not force and os.path.exists(obj) and os.path.exists(ostamp) and os.path.exists(obj + ".ptxas.txt")
+                and open(ostamp).read() == odg):
+            return obj, open(obj + ".ptxas.txt").read()
         cmd = [NVCC] + ARCH + FLAGS + list(defines) + ["-Xptxas", "-v", "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
         with open(obj + ".ptxas.txt", "w") as f:   # register / spill report, see ptxas_report()
             f.write(r.stderr)
+        with open(ostamp, "w") as f:
+            f.write(odg)
         return obj, r.stderr
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:

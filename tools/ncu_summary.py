@@ -22,3 +22,21 @@ for path in sys.argv[1:]:
             if w in h:
                 i = h.index(w)
                 print(f'  {w:78s} {row[i]:>18s} {u[i]}')
+        # every other warp-stall reason above 0.5 per issue, plus instruction / shared-memory counts
+        for i, w in enumerate(h):
+            if w in WANT:
+                continue
+            ok = ('issue_stalled' in w and w.endswith('per_issue_active.ratio')) or w in (
+                'smsp__inst_executed.sum', 'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum',
+                'l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum', 'l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum',
+                'sm__warps_active.avg.per_cycle_active', 'launch__occupancy_limit_registers',
+                'launch__occupancy_limit_shared_mem', 'sm__maximum_warps_per_active_cycle_pct')
+            if not ok:
+                continue
+            try:
+                v = float(row[i].replace(',', ''))
+            except ValueError:
+                continue
+            if 'issue_stalled' in w and v < 0.5:
+                continue
+            print(f'  {w:78s} {row[i]:>18s} {u[i]}')
