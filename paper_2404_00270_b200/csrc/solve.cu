@@ -62,6 +62,15 @@ struct BcsrOps {
     col = ld_nc_hint(&arc[p].x, pf);
     cf = ld_cg(&arc[ld_nc_hint(mate + p, pf)].y);
   }
+  // the same in-arc in two steps (top-down BFS): the neighbour and a key, then c_f(col -> w)
+  // only for neighbours still unlabelled (most in-arcs of later levels point at labelled
+  // vertices, so their c_f[mate] gather is skipped)
+  __device__ void in_arc_col(const Seg& s, int i, int& col, int& key) const {
+    const int p = s.fb + i;
+    col = ld_nc_hint(&arc[p].x, pf);
+    key = ld_nc_hint(mate + p, pf);
+  }
+  __device__ int in_cf(int key) const { return ld_cg(&arc[key].y); }
   __device__ void col_cf_of_slot(int slot, int& col, int& cf) const {
     int2 a = ld_cg(arc + slot); col = a.x; cf = a.y;
   }
@@ -139,7 +148,13 @@ struct RcsrOps {
       col = r.x;
       cf = ld_cg(&farc[r.y].y);
     }
+  }  __device__ void in_arc_col(const Seg& s, int i, int& col, int& key) const {
+    const int df = s.fe - s.fb;
+    if (i < df) { const int p = s.fb + i; col = ld_nc_hint(&farc[p].x, pf); key = ~p; }   // c_f = bcf[p]
+    else { const int2 r = ld_nc_hint(rarc + s.rb + (i - df), pf); col = r.x; key = r.y; }  // c_f = farc[f].y
   }
+  __device__ int in_cf(int key) const { return key < 0 ? ld_cg(bcf + ~key) : ld_cg(&farc[key].y); }
+
   __device__ void col_cf_of_slot(int slot, int& col, int& cf) const {
     if (slot < Mf) { int2 a = ld_cg(farc + slot); col = a.x; cf = a.y; }
     else { int2 r = __ldg(rarc + (slot - Mf)); col = r.x; cf = ld_cg(bcf + r.y); }
@@ -178,6 +193,9 @@ WBPR_DEV void st_release_v4(Bcast* p, uint4 v) {
                "r"(v.w) : "memory");
 }
 
+#ifndef WBPR_TD_LAZY
+#define WBPR_TD_LAZY 1   // top-down BFS: c_f(col -> w) loaded only for unlabelled neighbours
+#endif
 constexpr int kSmallCap = 2048;   // small-frontier mode: shared-memory queue capacity
 #ifndef WBPR_SMALL_MAX
 #define WBPR_SMALL_MAX 512
@@ -717,6 +735,19 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
   auto td_warp_scan = [&](const Seg& sg, int lo, int hi, const QueueOut& o, unsigned& fedges) {
     for (int b = lo; b < hi; b += 32 * kRU) {
       int u[kRU], cf[kRU], hu[kRU];
+#if WBPR_TD_LAZY
+      int mk[kRU];
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) {
+        const int i = b + j * 32 + lane;
+        u[j] = 0; mk[j] = 0;
+        if (i < hi) ops.in_arc_col(sg, i, u[j], mk[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) hu[j] = (b + j * 32 + lane < hi) ? ld_h(P.h + u[j], pl) : -1;
+#pragma unroll
+      for (int j = 0; j < kRU; ++j) cf[j] = hu[j] == N ? ops.in_cf(mk[j]) : 0;   // only unlabelled neighbours
+#else
 #pragma unroll
       for (int j = 0; j < kRU; ++j) {
         const int i = b + j * 32 + lane;
@@ -725,6 +756,7 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
       }
 #pragma unroll
       for (int j = 0; j < kRU; ++j) hu[j] = (b + j * 32 + lane < hi) ? ld_h(P.h + u[j], pl) : -1;   // with c_f (parallel)
+#endif
       bool found[kRU];
 #pragma unroll
       for (int j = 0; j < kRU; ++j)   // sinks 0, sources N+1: never N; level(u) = level(w) + 1
@@ -1137,14 +1169,27 @@ __global__ void __launch_bounds__(kSolveThreads, MINB) k_solve(const SolveParams
               int u[kBuB], cf[kBuB];
               // (16-B vector loads of the in-arcs, as the bottom-up scan does for out-arcs, were
               //  measured slower here: the c_f gathers dominate and the selects cost issue slots)
+              int hu[kBuB];
+#if WBPR_TD_LAZY
+              int mk[kBuB];
+#pragma unroll
+              for (int j = 0; j < kBuB; ++j) {
+                u[j] = 0; mk[j] = 0;
+                if (b0 + j < dthr) ops.in_arc_col(sw, b0 + j, u[j], mk[j]);
+              }
+#pragma unroll
+              for (int j = 0; j < kBuB; ++j) hu[j] = (b0 + j < dthr) ? ld_h(P.h + u[j], pl) : -1;
+#pragma unroll
+              for (int j = 0; j < kBuB; ++j) cf[j] = hu[j] == N ? ops.in_cf(mk[j]) : 0;   // only unlabelled neighbours
+#else
 #pragma unroll
               for (int j = 0; j < kBuB; ++j) {
                 u[j] = 0; cf[j] = 0;
                 if (b0 + j < dthr) ops.in_arc(sw, b0 + j, u[j], cf[j]);
               }
-              int hu[kBuB];
 #pragma unroll
               for (int j = 0; j < kBuB; ++j) hu[j] = (b0 + j < dthr) ? ld_h(P.h + u[j], pl) : -1;   // with c_f (parallel)
+#endif
               bool found[kBuB];
 #pragma unroll
               for (int j = 0; j < kBuB; ++j) found[j] = cf[j] > 0 && hu[j] == N && atomicCAS(P.h + u[j], N, level + 1) == N;
