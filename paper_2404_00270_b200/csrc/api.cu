@@ -625,8 +625,12 @@ wbpr_status solve_impl(const wbpr_csr* g, int k, const int64_t* vbase_h, const i
   }
   CK(cudaEventRecord(E.ev[2], st));
 
+  // the cut bitmap is always built (in queue scratch when the caller wants none or wants it on
+  // the host): the certificate looks the sides up in it (n/8 bytes instead of the labels);
+  // q0 holds the exported AVQ of debug_stop solves, so a bitmap nobody asked for goes to q1
   uint32_t* dbm = bitmap;
   if (bitmap && g->on_host) dbm = reinterpret_cast<uint32_t*>(at<int>(ws, L.q0));
+  if (!bitmap) dbm = reinterpret_cast<uint32_t*>(at<int>(ws, L.q1));
   long long* d_flow = at<long long>(ws, L.inst_flow);
   long long* d_cut = at<long long>(ws, L.inst_cut);
   {

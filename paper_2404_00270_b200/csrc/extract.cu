@@ -22,12 +22,16 @@ __global__ void k_bitmap(const int* __restrict__ h, int n, int N, uint32_t* bitm
 }
 
 // One warp per kCutChunk consecutive input edges as rows of 32 (coalesced col/cap loads,
-// owners by warp_owner); h(v) is gathered only for edges leaving S*.
+// owners by warp_owner); the side of v is looked up only for edges leaving S*, in the cut
+// bitmap when there is one (n/8 bytes: L1/L2-resident, where h is 4n bytes of random gathers).
 constexpr int kCutChunk = 32 * 64;
+__device__ __forceinline__ bool in_s(const uint32_t* __restrict__ bm, const int* __restrict__ h, int N, int v) {
+  return bm ? ((__ldg(bm + (v >> 5)) >> (v & 31)) & 1u) != 0 : ld_cg(h + v) >= N;
+}
 __global__ void __launch_bounds__(256) k_cutcap(const int64_t* __restrict__ ro, const int32_t* __restrict__ col,
                                                 const int32_t* __restrict__ cap, int64_t n, int64_t m,
-                                                const int* __restrict__ h, int N, const int64_t* __restrict__ vbase,
-                                                int k, long long* cut) {
+                                                const int* __restrict__ h, int N, const uint32_t* __restrict__ bm,
+                                                const int64_t* __restrict__ vbase, int k, long long* cut) {
   const int lane = lane_id();
   const int64_t E0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * kCutChunk;
   if (E0 >= m) return;
@@ -44,10 +48,10 @@ __global__ void __launch_bounds__(256) k_cutcap(const int64_t* __restrict__ ro, 
     const int u = warp_owner(ro, (int)n, ucur, ok ? i : E1 - 1);
     ucur = __shfl_sync(FULL, u, 31);
     if (!ok) continue;
-    if (ld_cg(h + u) < N) continue;        // u not in S*: the edge is not cut (skips col/cap)
+    if (!in_s(bm, h, N, u)) continue;      // u not in S*: the edge is not cut (skips col/cap)
     const int v = __ldg(col + i);
     const int c = __ldg(cap + i);
-    if (ld_cg(h + v) < N) {
+    if (!in_s(bm, h, N, v)) {
       if (u < ilo || u >= ihi) {
         if (acc) atomicAdd((unsigned long long*)(cut + inst), (unsigned long long)acc);
         acc = 0;
@@ -79,7 +83,7 @@ void extract_results(const SolveParams& p, const int64_t* ro, const int32_t* col
   cudaMemsetAsync(inst_cut, 0, sizeof(long long) * k, st);
   if (m > 0) {
     int64_t threads = (m + kCutChunk - 1) / kCutChunk * 32;
-    { k_cutcap<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(ro, col, cap, p.n, m, p.h, p.n, vbase, k, inst_cut); note_launch(); }
+    { k_cutcap<<<(unsigned)((threads + T - 1) / T), T, 0, st>>>(ro, col, cap, p.n, m, p.h, p.n, bitmap, vbase, k, inst_cut); note_launch(); }
   }
   { k_flows<<<(k + T - 1) / T, T, 0, st>>>(p.e, p.snk, k, inst_flow); note_launch(); }
 }
