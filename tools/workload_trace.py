@@ -54,6 +54,33 @@ def fit_eq1(rows):
     return coef, r2, rel
 
 
+def fit_rounds(rows):
+    """Eq. 1 at the level it is stated: a round's time is the max over tiles of the
+    summed local-operation costs, plus a fixed per-round term (barrier, launch of the round's
+    dependent memory chain) that the warp-level fit cannot see.  Regress each round's measured
+    time (max busy_ns over its warps) on c0 + k * slots_w* + P * pushes_w* + R * relabels_w*,
+    where w* is the round's most loaded warp by slots (non-negative least squares, leave-one-out
+    R^2 so the intercept cannot fit noise)."""
+    from scipy.optimize import nnls
+    X, y = [], []
+    for act in rows:
+        w = int(np.argmax(act["slots"]))
+        X.append([1.0, act["slots"][w], act["pushes"][w], act["relabels"][w]])
+        y.append(float(act["busy_ns"].max()))
+    X, y = np.array(X, np.float64), np.array(y)
+    coef, _ = nnls(X, y)
+    if len(y) < 4:
+        return coef, float("nan")
+    pred = np.empty_like(y)
+    for i in range(len(y)):
+        m = np.ones(len(y), bool)
+        m[i] = False
+        c, _ = nnls(X[m], y[m])
+        pred[i] = X[i] @ c
+    r2 = 1 - ((y - pred) ** 2).sum() / max(((y - y.mean()) ** 2).sum(), 1e-9)
+    return coef, float(r2)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rounds", type=int, default=24)
@@ -62,8 +89,9 @@ def main():
               ("R-MAT-18 paper rule", synth.rmat(18, 16, 1000, "paper")),
               ("grid 256x256 U[1,100] (road-like)", synth.grid(256, 256, True, 1))]
     print("| graph | schedule | traced rounds | busy/mean stddev (median) | max/mean (median) | "
-          "Eq.1 k ns/slot | P ns/push | R ns/relabel | Eq.1 round-time R^2 | median rel. err |")
-    print("|---|---|---|---|---|---|---|---|---|---|")
+          "Eq.1 k ns/slot | P ns/push | R ns/relabel | Eq.1 round-time R^2 | median rel. err | "
+          "round-level fit c0 us / k ns/slot | round-level LOO R^2 |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for name, g in graphs:
         ro, col, cap = (torch.from_numpy(x).cuda() for x in (g.row_off, g.col, g.cap))
         for sch in ("tc", "vc"):
@@ -75,9 +103,10 @@ def main():
             if not an["rows"]:
                 continue
             coef, r2, rel = fit_eq1(an["rows"])
+            rc, rr2 = fit_rounds(an["rows"])
             print(f"| {name} | {sch.upper()} | {len(an['rows'])} | {np.median(an['std']):.3f} | "
-                  f"{np.median(an['maxmean']):.2f} | {coef[1]:.2f} | {coef[2]:.1f} | {coef[3]:.1f} | {r2:.3f} | {rel:.3f} |",
-                  flush=True)
+                  f"{np.median(an['maxmean']):.2f} | {coef[1]:.2f} | {coef[2]:.1f} | {coef[3]:.1f} | {r2:.3f} | {rel:.3f} | "
+                  f"{rc[0] / 1e3:.2f} / {rc[1]:.2f} | {rr2:.3f} |", flush=True)
 
 
 if __name__ == "__main__":
