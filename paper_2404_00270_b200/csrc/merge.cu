@@ -262,6 +262,7 @@ __device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int 
 __global__ void __launch_bounds__(256) k_merge_warp(MergeArgs a) {
   const int cnt = a.ctrl->mlist_w;
   const int lane = lane_id();
+  long long msum = 0;   // slots written by this warp (ctrl->M)
   int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int nw = (gridDim.x * blockDim.x) >> 5;
 #if WBPR_MERGE_PF
@@ -284,9 +285,12 @@ __global__ void __launch_bounds__(256) k_merge_warp(MergeArgs a) {
 #endif
     const int base = ob + ib;   // gapped layout (see k_merge_thread)
     int h = warp_merge_range<1>(a, ob, lo, ib, li, 0, 0, 0, lo + li, kInf, base);
-    if (lane == 0) { a.seg[x] = make_int2(base, base + h); atomicAdd(&a.ctrl->M, h); }
+    if (lane == 0) a.seg[x] = make_int2(base, base + h);
+    msum += h;
     for (int g = base + h + lane; g < base + lo + li; g += 32) a.arc[g] = make_int2(0, 0);   // unused tail
   }
+  // one slot-count atomic per warp, not per vertex (millions of same-address atomics serialise)
+  if (lane == 0 && msum) atomicAdd(&a.ctrl->M, (int)msum);
 }
 
 // global co-rank on the full lists (Out compared by column)

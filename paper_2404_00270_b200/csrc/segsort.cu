@@ -167,16 +167,22 @@ __global__ void __launch_bounds__(256) k_sort_med(K* keys, const int2* __restric
 
 // Enumerate sort items: 32 < len <= 256 -> warp items; 256 < len <= tile -> CTA item;
 // longer segments -> ceil(len/tile) CTA chunk items and the `big` list.
+// (medium items are appended with one atomic per warp: they are numerous, and same-address
+// atomics from every thread serialise)
 __global__ void k_sort_items(const int* __restrict__ off, int nseg, const uint8_t* __restrict__ need,
                              int2* items, int2* items_med, int* big, Ctrl* ctrl, int medmax) {
-  for (int sgi = blockIdx.x * blockDim.x + threadIdx.x; sgi < nseg; sgi += gridDim.x * blockDim.x) {
-    if (need && !need[sgi]) continue;
-    int beg = off[sgi], len = off[sgi + 1] - beg;
-    if (len <= 32) continue;
-    if (len <= medmax) {
-      items_med[atomicAdd(&ctrl->sort_items_med, 1)] = make_int2(beg, len);
-      continue;
-    }
+  const int lane = lane_id();
+  for (int base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; base < nseg; base += gridDim.x * blockDim.x) {
+    const int sgi = base + lane;
+    int beg = 0, len = 0;
+    if (sgi < nseg && (!need || need[sgi])) { beg = off[sgi]; len = off[sgi + 1] - beg; }
+    const bool med = len > 32 && len <= medmax;
+    const unsigned bm = __ballot_sync(FULL, med);
+    int pm = 0;
+    if (lane == 0 && bm) pm = atomicAdd(&ctrl->sort_items_med, __popc(bm));
+    pm = __shfl_sync(FULL, pm, 0);
+    if (med) items_med[pm + __popc(bm & ((1u << lane) - 1u))] = make_int2(beg, len);
+    if (len <= medmax) continue;
     int nit = (len + kSortTile - 1) / kSortTile;
     int idx = atomicAdd(&ctrl->sort_items, nit);
     for (int c = 0; c < nit; ++c) {
