@@ -199,9 +199,12 @@ __device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int 
                                                 int k0, int k1, uint32_t prev, int slot_base) {
   const int lane = lane_id();
   int heads = 0;
+  // register windows: 32 out-keys (column and capacity) and 32 in-list sources; the next
+  // window is loaded as soon as this one's consumption is known, before its stores
+  uint64_t ak = (k0 < k1 && i0 + lane < lo) ? a.outk[ob + i0 + lane] : kSentKey;
+  uint32_t bv = (k0 < k1 && j0 + lane < li) ? a.ink[ib + j0 + lane] : kInf;
   for (int produced = k0; produced < k1; produced += 32) {
-    uint32_t av = (i0 + lane < lo) ? kcol(a.outk[ob + i0 + lane]) : kInf;
-    uint32_t bv = (j0 + lane < li) ? a.ink[ib + j0 + lane] : kInf;
+    const uint32_t av = kcol(ak);
     int la = lo - i0 < 32 ? lo - i0 : 32;
     int lb = li - j0 < 32 ? li - j0 : 32;
     if (la < 0) la = 0;
@@ -222,6 +225,8 @@ __device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int 
     int i = rlo, j = k - rlo;
     uint32_t Ai = __shfl_sync(FULL, av, i & 31);
     uint32_t Bj = __shfl_sync(FULL, bv, j & 31);
+    const uint64_t Aki = __shfl_sync(FULL, ak, i & 31);            // A[i] with its capacity
+    const uint32_t Ai1 = __shfl_sync(FULL, av, (i + 1) & 31);      // A[i + 1] (parallel edge?)
     bool takeA = j >= lb || (i < la && Ai <= Bj);
     uint32_t c = takeA ? Ai : Bj;
     bool valid = produced + lane < k1 && c != kInf;
@@ -229,6 +234,15 @@ __device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int 
     if (lane == 0) pc = prev;
     bool head = valid && c != pc;
     unsigned hm = __ballot_sync(FULL, head);
+    const int nA = __shfl_sync(FULL, i + (takeA ? 1 : 0), 31);
+    const uint32_t last = __shfl_sync(FULL, c, 31);
+    const int i0n = i0 + nA, j0n = j0 + 32 - nA;
+    uint64_t akn = kSentKey;
+    uint32_t bvn = kInf;
+    if (produced + 32 < k1) {   // (warp-uniform)
+      akn = i0n + lane < lo ? a.outk[ob + i0n + lane] : kSentKey;
+      bvn = j0n + lane < li ? a.ink[ib + j0n + lane] : kInf;
+    }
     if (PASS == 1 && valid) {
       // slot of this output's run: the last head at or before this lane (a run without a
       // head in this window continues the previous window's last slot)
@@ -239,19 +253,23 @@ __device__ __forceinline__ int warp_merge_range(const MergeArgs& a, int ob, int 
     if (PASS == 1 && head) {
       long long sum = 0;
       if (takeA) {
-        for (int q = i0 + i; q < lo; ++q) {
-          uint64_t kk = a.outk[ob + q];
-          if (kcol(kk) != c) break;
-          sum += kcap(kk);
-        }
+        sum = kcap(Aki);
+        // parallel edges: the run continues past A[i] (rare; from global memory)
+        if (i + 1 >= la || Ai1 == c)
+          for (int q = i0 + i + 1; q < lo; ++q) {
+            uint64_t kk = a.outk[ob + q];
+            if (kcol(kk) != c) break;
+            sum += kcap(kk);
+          }
       }
       emit(a, slot_base + heads + __popc(hm & ((1u << lane) - 1u)), c, sum);
     }
     heads += __popc(hm);
-    int nA = __shfl_sync(FULL, i + (takeA ? 1 : 0), 31);
-    prev = __shfl_sync(FULL, c, 31);
-    i0 += nA;
-    j0 += 32 - nA;
+    prev = last;
+    i0 = i0n;
+    j0 = j0n;
+    ak = akn;
+    bv = bvn;
   }
   return heads;
 }
