@@ -153,10 +153,12 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
     // before x bounds the distinct columns before x), so no counting pass is needed
     int i = 0, j = 0, r = 0;
     const int slot0 = ob + ib;
-    // two-pointer merge; each element is loaded once, the next head of a list is loaded as
-    // soon as its current one is consumed (one dependent load per consumed element)
+    // two-pointer merge; each element is loaded once, one element ahead of its use in each
+    // list (a consumed head's successor is already in flight)
     uint64_t ka = lo > 0 ? a.outk[ob] : kSentKey;
+    uint64_t ka2 = lo > 1 ? a.outk[ob + 1] : kSentKey;
     uint32_t kb = li > 0 ? a.ink[ib] : kInf;
+    uint32_t kb2 = li > 1 ? a.ink[ib + 1] : kInf;
     while (true) {
       uint32_t ca = kcol(ka);
       const uint32_t c = ca < kb ? ca : kb;
@@ -166,13 +168,15 @@ __global__ void __launch_bounds__(256) k_merge_thread(MergeArgs a) {
         sum += kcap(ka);
         if (PASS == 1) a.outslot[ob + i] = slot0 + r;
         ++i;
-        ka = i < lo ? a.outk[ob + i] : kSentKey;
+        ka = ka2;
+        ka2 = i + 1 < lo ? a.outk[ob + i + 1] : kSentKey;
         ca = kcol(ka);
       }
       while (kb == c) {
         if (PASS == 1) a.inslot[ib + j] = slot0 + r;
         ++j;
-        kb = j < li ? a.ink[ib + j] : kInf;
+        kb = kb2;
+        kb2 = j + 1 < li ? a.ink[ib + j + 1] : kInf;
       }
       if (PASS == 1) emit(a, slot0 + r, c, sum);
       ++r;
