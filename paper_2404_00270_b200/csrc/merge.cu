@@ -16,7 +16,7 @@
 //   * the merge records the slot of every out-half-arc (outslot[e]) and of every in-list
 //     entry (inslot[t]); mate[] is then one lookup per input edge (build.cu k_mate) -
 //     the paper's backward-arc binary search is never run.
-// Merge classes: <= 32 elements: one thread, sequential two-pointer merge;
+// Merge classes: <= kMergeThreadMax (12) elements: one thread, sequential two-pointer merge;
 // <= 8192: one warp, merge path advanced 32 outputs at a time with the 32-element
 // windows of both lists held in registers (co-rank by shuffles); larger: split into
 // 4096-output warp tasks whose starts come from a global co-rank search (their counts
@@ -30,7 +30,10 @@ namespace wbpr {
 
 constexpr uint64_t kSentKey = ~0ull;
 constexpr uint32_t kInf = 0xffffffffu;
-constexpr int kMergeThreadMax = 32;
+#ifndef WBPR_MERGE_TMAX
+#define WBPR_MERGE_TMAX 12   // measured (profiles/r2/ab_merge_tmax.txt): 32 -> 16 -> 12: C5 build 20.64 -> 20.49 ms, C4 4.23 -> 4.04 ms
+#endif
+constexpr int kMergeThreadMax = WBPR_MERGE_TMAX;
 constexpr int kMergeWarpMax = 8192;
 constexpr int kMergeChunk = 4096;
 
