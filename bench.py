@@ -663,7 +663,7 @@ def run_wbpr(args, rank, world, local_rank):
             parity["instances"] += 1
         secs = [res[k_][3] for k_ in batch_keys]
         nb_ = len(batch_keys)
-        if rank == 0:
+        if rank == 0 and world == 1:   # (the contract's cpu_baseline is N = 1 only; the parity gate runs at every N)
             cpu = {"value": round(nb_ / wall, 4), "unit": "instances/s" if wl["kind"] == "batch" else "solves/s",
                    "cores": min(pool.workers, nb_), "kind": "oracle",
                    "sample": f"every instance of this rank's workload ({nb_}), oracle solve on a process pool of "
