@@ -31,7 +31,43 @@ def _build(g, layout):
 
 
 BUILD_CASES = [("tiny", s) for s in range(12)] + [("c1", 1), ("grid", 1), ("rmat", 3), ("hubs", 0),
-                                                  ("sorted_rmat", 4), ("bip", 1)]
+                                                  ("sorted_rmat", 4), ("bip", 1)] + [("runs", s) for s in range(3)]
+
+
+def _runs_graph(seed):
+    """Segments sized around the merge-class boundaries (thread class <= 12 elements, warp
+    windows of 32 outputs, 64, 96) with runs of parallel and antiparallel half-arcs placed
+    across the 32-output window boundaries: the warp merge's register run sums and their
+    global continuation, and the next-window prefetch (merge.cu)."""
+    rng = np.random.default_rng(100 + seed)
+    n = 600
+    src, dst = [], []
+    for p_, size in enumerate([11, 12, 13, 14, 20, 31, 32, 33, 34, 40, 63, 64, 65, 96, 97, 130]):
+        u = p_
+        d_in = size // 3
+        cols = list(rng.choice(np.arange(200, n), size=size - d_in, replace=False))
+        # parallel copies of the columns that land around output positions 28-36 and 60-68
+        sc = sorted(cols)
+        for k in (27, 29, 30, 31, 32, 33, 62, 63, 64):
+            if k < len(sc):
+                cols += [sc[k]] * int(rng.integers(1, 3))
+        for c in cols:
+            src.append(u); dst.append(c)
+        # in-arcs: some antiparallel (from columns u points to), some from elsewhere
+        ins = list(rng.choice(sc, size=min(d_in // 2, len(sc)), replace=False)) + \
+            list(rng.integers(20, n, size=d_in - d_in // 2))
+        for v in ins:
+            src.append(int(v)); dst.append(u)
+            if rng.random() < 0.3:
+                src.append(int(v)); dst.append(u)    # parallel in-edge
+    # background edges so that s and t connect through the probe vertices
+    for _ in range(3000):
+        a, b = rng.integers(0, n, 2)
+        if a != b:
+            src.append(int(a)); dst.append(int(b))
+    src, dst = np.array(src, np.int64), np.array(dst, np.int64)
+    cap = rng.integers(0, 60, src.shape[0]).astype(np.int32)
+    return synth.shuffle_rows(synth.from_edges(n, src, dst, cap, 0, n - 1, name=f"runs{seed}"), seed)
 
 
 def _build_graph(kind, seed):
@@ -54,6 +90,8 @@ def _build_graph(kind, seed):
                               np.full(12000, 2)])
         cap = rng.integers(0, 50, src.shape[0]).astype(np.int32)
         return synth.shuffle_rows(synth.from_edges(n, src, dst, cap, 0, n - 1), 3)
+    if kind == "runs":
+        return _runs_graph(seed)
     if kind == "sorted_rmat":   # rows already column-sorted (no out-row sort needed)
         return synth.rmat(12, 16, seed, "paper")
     if kind == "bip":           # 2^12 x 2^12 matching network: s and t are hubs
@@ -355,3 +393,11 @@ def test_async_gr_deep_graphs(layout, kind):
     F, st = assert_parity(g, layout, bfs_mode=3)
     if kind != "path":
         assert st["phase_count"][7] > 0, "the asynchronous continuation did not run"
+
+
+@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_runs_across_merge_windows_parity(seed, layout):
+    """F, cut capacity and bitmap bit-exact on the merge-class boundary graphs (parallel and
+    antiparallel runs across the warp-merge windows), and V1-V7 on the residual state."""
+    assert_parity(_runs_graph(seed), layout)
