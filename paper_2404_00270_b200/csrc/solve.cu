@@ -148,13 +148,13 @@ struct RcsrOps {
       col = r.x;
       cf = ld_cg(&farc[r.y].y);
     }
-  }  __device__ void in_arc_col(const Seg& s, int i, int& col, int& key) const {
+  }
+  __device__ void in_arc_col(const Seg& s, int i, int& col, int& key) const {
     const int df = s.fe - s.fb;
     if (i < df) { const int p = s.fb + i; col = ld_nc_hint(&farc[p].x, pf); key = ~p; }   // c_f = bcf[p]
     else { const int2 r = ld_nc_hint(rarc + s.rb + (i - df), pf); col = r.x; key = r.y; }  // c_f = farc[f].y
   }
   __device__ int in_cf(int key) const { return key < 0 ? ld_cg(bcf + ~key) : ld_cg(&farc[key].y); }
-
   __device__ void col_cf_of_slot(int slot, int& col, int& cf) const {
     if (slot < Mf) { int2 a = ld_cg(farc + slot); col = a.x; cf = a.y; }
     else { int2 r = __ldg(rarc + (slot - Mf)); col = r.x; cf = ld_cg(bcf + r.y); }
